@@ -1,0 +1,149 @@
+/*
+ * sieve.h -- C ABI of libsieve.so, the B200 (sm_100a) segmented sieve of
+ * Eratosthenes.
+ *
+ * The operation (Sec. 3.1 "Algorithm Design"): "iteratively
+ * marking as composite the multiples of each prime, starting with the
+ * multiples of 2", applied to a contiguous range of integers that is split
+ * into blocks ("average divide data into nodes"; Eq. 3,
+ * PAPER.md:133-135).  The survivors are the primes, i.e. the integers n >= 2
+ * with no divisor d in [2, sqrt(n)].  pi(x), the count of
+ * primes, is the paper's PAPER.md:36 quantity.
+ *
+ * Conventions:
+ *   R1  every range is HALF-OPEN [lo, hi); lo == hi is empty (not an error).
+ *       Valid: lo <= hi <= SIEVE_MAX_HI (2^48).
+ *   R2  0 and 1 are not prime; 2 is prime and is counted/summed/listed, but
+ *       it is not in the odd-only bitmap.
+ *   R5  bitmap: bit j (0 <= j < B, B = hi/2 - lo/2) of uint32 word j>>5,
+ *       LSB first, is 1 iff the odd integer (lo|1) + 2j is prime.  Padding
+ *       bits of the last word are 0.  Length sieve_bitmap_words(lo, hi).
+ *   R7  sum = (sum of all primes in [lo, hi)) mod 2^64 (wrapping).
+ *   R8  list = the primes in [lo, hi) ascending as uint64.
+ *
+ * Ownership and memory: output pointers are owned by the caller and may be
+ * HOST or DEVICE memory (detected with cudaPointerGetAttributes).  Device
+ * outputs are written in place on the library stream; host outputs receive a
+ * device->host copy.  The library owns device scratch (base primes, partials,
+ * list staging) and keeps it until sieve_shutdown().
+ *
+ * Threading: the synchronous calls return only after the GPU work finished.
+ * All entry points are serialized by one internal mutex.  No C++ exception
+ * ever crosses the ABI; failures return a negative SIEVE_E* code and set a
+ * thread-local message readable with sieve_last_error().
+ *
+ * There is NO CPU fallback: without a usable CUDA device every compute call
+ * returns SIEVE_ENODEV.
+ */
+#ifndef PAPER_1205_4883_B200_SIEVE_H
+#define PAPER_1205_4883_B200_SIEVE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIEVE_MAX_HI ((uint64_t)1 << 48)
+
+/* error codes (all negative) */
+#define SIEVE_OK 0
+#define SIEVE_EINVAL -1 /* lo > hi, NULL output with non-zero size, bad option */
+#define SIEVE_ERANGE -2 /* hi > SIEVE_MAX_HI */
+#define SIEVE_ENOMEM -3 /* device or host allocation failed */
+#define SIEVE_ECUDA -4  /* a CUDA runtime call or kernel launch failed */
+#define SIEVE_ENODEV -5 /* no CUDA device / driver available */
+
+/* Tuning options (sieve_set_options).  Zero fields mean "default". */
+typedef struct sieve_options {
+    uint32_t segment_kb;  /* shared-memory segment size in KiB: 32, 64, 128 or 192 (default 192) */
+    uint32_t wheel;       /* wheel bound w (pre-sieved primes 3..w): 19, 29, 37, 43, 53 or 61 (default 43) */
+    uint32_t ctas_per_sm; /* resident CTAs per SM for the sieve kernel (default: occupancy maximum) */
+    uint32_t threads;     /* threads per CTA: 256, 512 or 1024 (default 1024) */
+    uint32_t reserved[4]; /* must be zero */
+} sieve_options;
+
+/* ---------------------------------------------------------------------- */
+/* The three calls named by north_star (BASELINE.json:5).                 */
+/* ---------------------------------------------------------------------- */
+
+/* pi(hi-1) - pi(lo-1): the number of primes in [lo, hi).  >= 0, or < 0 error. */
+int64_t sieve_count(uint64_t lo, uint64_t hi);
+
+/* Writes the odd-only prime bitmap of [lo, hi) (reading R5) into `out`
+ * (sieve_bitmap_words(lo, hi) uint32 words, host or device).  Returns the
+ * prime count (2 included when in range), or < 0 on error.  `out` may be
+ * NULL only when the range holds no odd integer. */
+int64_t sieve_bitmap(uint64_t lo, uint64_t hi, uint32_t *out);
+
+/* Writes the min(count, cap) smallest primes of [lo, hi), ascending, into
+ * `out` (uint64, host or device).  Returns the TOTAL count (> cap means the
+ * list was truncated), or < 0 on error.  out may be NULL iff cap == 0, which
+ * is a size query. */
+int64_t sieve_primes(uint64_t lo, uint64_t hi, uint64_t *out, uint64_t cap);
+
+/* ---------------------------------------------------------------------- */
+/* Extensions the configs need.                        */
+/* ---------------------------------------------------------------------- */
+
+/* ceil((hi/2 - lo/2) / 32); 0 for an empty or odd-free range. */
+uint64_t sieve_bitmap_words(uint64_t lo, uint64_t hi);
+
+/* count and (sum of primes) mod 2^64 of [lo, hi) into host pointers. */
+int sieve_stats(uint64_t lo, uint64_t hi, uint64_t *count, uint64_t *sum_mod_2_64);
+
+/* n independent intervals [lo[i], hi[i]) (host arrays); per-interval count
+ * and sum mod 2^64 written to host arrays in input order (config 5). */
+int sieve_batch(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t *count,
+                uint64_t *sum_mod_2_64);
+
+/* ---------------------------------------------------------------------- */
+/* Device-resident, stream-ordered API (multi-GPU orchestration, bench).   */
+/* All pointers below are DEVICE pointers; calls enqueue work on the        */
+/* library stream and return without synchronizing.                        */
+/* ---------------------------------------------------------------------- */
+
+/* Upper bound on the number of odd primes <= r (sizes base-prime buffers). */
+uint64_t sieve_base_capacity(uint64_t r);
+
+/* Base primes (step A2): the odd primes p <= r ascending into primes[],
+ * their Barrett reciprocals floor((2^64-1)/p) into recips[] and the count
+ * into *nbase.  cap must be >= sieve_base_capacity(r).  r <= 2^24. */
+int sieve_base_primes_async(uint64_t r, uint32_t *primes, uint64_t *recips, uint64_t cap,
+                            uint32_t *nbase);
+
+/* Recomputes recips[] for primes[] received from elsewhere (e.g. an NCCL
+ * broadcast of primes[] and *nbase). */
+int sieve_prepare_base_async(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
+                             uint64_t cap);
+
+/* Count mode on [lo, hi) with the given base primes (all odd primes up to
+ * at least isqrt(hi-1) must be present; larger ones are ignored).  Writes
+ * result[0] = count, result[1] = sum mod 2^64 (overwrites). */
+int sieve_stats_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const uint64_t *recips,
+                      const uint32_t *nbase, uint64_t *result);
+
+/* Bitmap mode: writes sieve_bitmap_words(lo,hi) words into out (device,
+ * 16-byte aligned for vector stores; any alignment accepted) and
+ * result[0..1] as above. */
+int sieve_bitmap_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const uint64_t *recips,
+                       const uint32_t *nbase, uint32_t *out, uint64_t *result);
+
+/* ---------------------------------------------------------------------- */
+/* Configuration and diagnostics.                                          */
+/* ---------------------------------------------------------------------- */
+int sieve_set_device(int ordinal);
+int sieve_set_stream(void *cuda_stream); /* NULL: the library's own stream */
+void *sieve_get_stream(void);
+int sieve_set_options(const sieve_options *o); /* NULL resets defaults */
+int sieve_get_options(sieve_options *o);
+const char *sieve_last_error(void);
+void sieve_shutdown(void);
+
+/* Number of kernels this library launched since load (evidence counter). */
+uint64_t sieve_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,204 @@
+"""ctypes binding of libsieve.so -- one Python function per C entry point of
+include/sieve.h, same names without the ``sieve_`` prefix.  Marshalling only.
+
+Host outputs are numpy arrays; device outputs are torch CUDA tensors (their
+``data_ptr()`` is passed straight through).  torch is imported lazily and is
+needed only for the device-resident ``*_async`` calls.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(_HERE, "libsieve.so")
+
+SIEVE_MAX_HI = 1 << 48
+_ERRNAMES = {-1: "SIEVE_EINVAL", -2: "SIEVE_ERANGE", -3: "SIEVE_ENOMEM", -4: "SIEVE_ECUDA",
+             -5: "SIEVE_ENODEV"}
+
+_u64 = ctypes.c_uint64
+_i64 = ctypes.c_int64
+_p = ctypes.c_void_p
+
+
+class SieveError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("segment_kb", ctypes.c_uint32), ("wheel", ctypes.c_uint32),
+                ("ctas_per_sm", ctypes.c_uint32), ("threads", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32 * 4)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsieve.so (built in-tree by ``__graft_entry__.build()`` / make)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(library_path):
+            raise ImportError(f"{library_path} is missing: run `make` or __graft_entry__.build()")
+        L = ctypes.CDLL(library_path)
+        sig = {
+            "sieve_count": (_i64, [_u64, _u64]),
+            "sieve_bitmap": (_i64, [_u64, _u64, _p]),
+            "sieve_primes": (_i64, [_u64, _u64, _p, _u64]),
+            "sieve_bitmap_words": (_u64, [_u64, _u64]),
+            "sieve_stats": (ctypes.c_int, [_u64, _u64, _p, _p]),
+            "sieve_batch": (ctypes.c_int, [_p, _p, _u64, _p, _p]),
+            "sieve_base_capacity": (_u64, [_u64]),
+            "sieve_base_primes_async": (ctypes.c_int, [_u64, _p, _p, _u64, _p]),
+            "sieve_prepare_base_async": (ctypes.c_int, [_p, _p, _p, _u64]),
+            "sieve_stats_async": (ctypes.c_int, [_u64, _u64, _p, _p, _p, _p]),
+            "sieve_bitmap_async": (ctypes.c_int, [_u64, _u64, _p, _p, _p, _p, _p]),
+            "sieve_set_device": (ctypes.c_int, [ctypes.c_int]),
+            "sieve_set_stream": (ctypes.c_int, [_p]),
+            "sieve_get_stream": (_p, []),
+            "sieve_set_options": (ctypes.c_int, [ctypes.POINTER(_Options)]),
+            "sieve_get_options": (ctypes.c_int, [ctypes.POINTER(_Options)]),
+            "sieve_last_error": (ctypes.c_char_p, []),
+            "sieve_shutdown": (None, []),
+            "sieve_kernel_launches": (_u64, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> int:
+    if rc < 0:
+        raise SieveError(rc, lib().sieve_last_error().decode())
+    return rc
+
+
+def _ptr(x) -> int | None:
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()  # torch tensor
+
+
+# ---- north_star calls -----------------------------------------------------
+def count(lo: int, hi: int) -> int:
+    """Number of primes in [lo, hi)."""
+    return _check(lib().sieve_count(lo, hi))
+
+
+def bitmap_words(lo: int, hi: int) -> int:
+    return int(lib().sieve_bitmap_words(lo, hi))
+
+
+def bitmap(lo: int, hi: int, out=None):
+    """Odd-only prime bitmap of [lo, hi) (uint32 words; reading R5).
+    ``out`` may be a numpy uint32 array (host) or a torch int32/uint32 CUDA
+    tensor (device).  Returns (out, count)."""
+    w = bitmap_words(lo, hi)
+    if out is None:
+        out = np.zeros(max(w, 1), dtype=np.uint32)
+    c = _check(lib().sieve_bitmap(lo, hi, _ptr(out) if w else None))
+    return out, c
+
+
+def primes(lo: int, hi: int, cap: int | None = None, out=None):
+    """Ascending uint64 primes of [lo, hi).  Returns (out, total_count)."""
+    if cap is None:
+        cap = count(lo, hi) if out is None else int(out.numel() if hasattr(out, "numel") else out.size)
+    if out is None:
+        out = np.zeros(max(cap, 1), dtype=np.uint64)
+    c = _check(lib().sieve_primes(lo, hi, _ptr(out) if cap else None, cap))
+    return out, c
+
+
+def stats(lo: int, hi: int) -> tuple[int, int]:
+    """(count, sum of primes mod 2^64) of [lo, hi)."""
+    c = ctypes.c_uint64()
+    s = ctypes.c_uint64()
+    _check(lib().sieve_stats(lo, hi, ctypes.addressof(c), ctypes.addressof(s)))
+    return int(c.value), int(s.value)
+
+
+def batch(lo, hi) -> tuple[np.ndarray, np.ndarray]:
+    """Per-interval (count, sum mod 2^64) of the intervals [lo[i], hi[i])."""
+    lo = np.ascontiguousarray(lo, dtype=np.uint64)
+    hi = np.ascontiguousarray(hi, dtype=np.uint64)
+    n = lo.size
+    c = np.zeros(max(n, 1), dtype=np.uint64)
+    s = np.zeros(max(n, 1), dtype=np.uint64)
+    _check(lib().sieve_batch(lo.ctypes.data, hi.ctypes.data, n, c.ctypes.data, s.ctypes.data))
+    return c[:n], s[:n]
+
+
+# ---- device-resident API ----------------------------------------------------
+def base_capacity(r: int) -> int:
+    return int(lib().sieve_base_capacity(r))
+
+
+def base_primes_async(r: int, primes_t, recips_t, nbase_t) -> None:
+    _check(lib().sieve_base_primes_async(r, _ptr(primes_t), _ptr(recips_t), primes_t.numel(),
+                                         _ptr(nbase_t)))
+
+
+def prepare_base_async(primes_t, nbase_t, recips_t) -> None:
+    _check(lib().sieve_prepare_base_async(_ptr(primes_t), _ptr(nbase_t), _ptr(recips_t),
+                                          primes_t.numel()))
+
+
+def stats_async(lo: int, hi: int, primes_t, recips_t, nbase_t, result_t) -> None:
+    _check(lib().sieve_stats_async(lo, hi, _ptr(primes_t), _ptr(recips_t), _ptr(nbase_t),
+                                   _ptr(result_t)))
+
+
+def bitmap_async(lo: int, hi: int, primes_t, recips_t, nbase_t, out_t, result_t) -> None:
+    _check(lib().sieve_bitmap_async(lo, hi, _ptr(primes_t), _ptr(recips_t), _ptr(nbase_t),
+                                    _ptr(out_t), _ptr(result_t)))
+
+
+# ---- configuration ----------------------------------------------------------
+def set_device(ordinal: int) -> None:
+    _check(lib().sieve_set_device(ordinal))
+
+
+def set_stream(stream) -> None:
+    """stream: a torch.cuda.Stream, a raw cudaStream_t int, or None."""
+    if stream is None:
+        h = None
+    elif isinstance(stream, int):
+        h = stream
+    else:
+        h = stream.cuda_stream
+    _check(lib().sieve_set_stream(h))
+
+
+def get_stream() -> int:
+    return int(lib().sieve_get_stream() or 0)
+
+
+def set_options(segment_kb: int = 0, wheel: int = 0, ctas_per_sm: int = 0, threads: int = 0) -> None:
+    o = _Options(segment_kb, wheel, ctas_per_sm, threads)
+    _check(lib().sieve_set_options(ctypes.byref(o)))
+
+
+def get_options() -> dict:
+    o = _Options()
+    _check(lib().sieve_get_options(ctypes.byref(o)))
+    return {"segment_kb": o.segment_kb, "wheel": o.wheel, "ctas_per_sm": o.ctas_per_sm,
+            "threads": o.threads}
+
+
+def shutdown() -> None:
+    lib().sieve_shutdown()
+
+
+def kernel_launches() -> int:
+    return int(lib().sieve_kernel_launches())

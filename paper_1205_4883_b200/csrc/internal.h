@@ -1,0 +1,101 @@
+// internal.h -- shared between the kernels (kernels.cu) and the host runtime
+// (runtime.cu) of libsieve.so.  Nothing here is visible through the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sv {
+
+// ---------------------------------------------------------------------------
+// Wheel pre-sieve groups (step A3).  Group g is a set of small odd primes
+// whose product P_g is the period of their composite pattern on the odd-only
+// grid.  Table g holds bit i = 1 iff the odd integer 2i+1 is divisible by a
+// prime of the group, for i in [0, P_g + kTablePad) so that any 160-bit
+// window starting below P_g can be read without wrapping.
+// ---------------------------------------------------------------------------
+constexpr int kMaxGroups = 7;
+constexpr uint32_t kTablePad = 160;
+__host__ __device__ constexpr uint32_t group_period(int g) {
+  return g == 0 ? 15015u   // 3*5*7*11*13
+       : g == 1 ? 323u     // 17*19
+       : g == 2 ? 667u     // 23*29
+       : g == 3 ? 1147u    // 31*37
+       : g == 4 ? 1763u    // 41*43
+       : g == 5 ? 2491u    // 47*53
+                : 3599u;   // 59*61
+}
+__host__ __device__ constexpr uint32_t group_words(int g) {
+  return (group_period(g) + kTablePad + 31) / 32;
+}
+__host__ __device__ constexpr uint32_t group_offset(int g) {
+  return g == 0 ? 0u : group_offset(g - 1) + group_words(g - 1);
+}
+__host__ __device__ constexpr uint32_t tables_words(int ng) { return group_offset(ng); }
+// largest prime covered by the first ng groups (the wheel bound w)
+__host__ __device__ constexpr uint32_t wheel_bound(int ng) {
+  return ng == 1 ? 13u : ng == 2 ? 19u : ng == 3 ? 29u : ng == 4 ? 37u : ng == 5 ? 43u : ng == 6 ? 53u : 61u;
+}
+// number of odd primes <= wheel_bound(ng): index of the first marking prime
+__host__ __device__ constexpr uint32_t wheel_nprimes(int ng) {
+  return ng == 1 ? 5u : ng == 2 ? 7u : ng == 3 ? 9u : ng == 4 ? 11u : ng == 5 ? 13u : ng == 6 ? 15u : 17u;
+}
+// bit n set iff n is an odd prime <= 61
+constexpr uint64_t kOddPrimesBelow64 =
+    (1ull << 3) | (1ull << 5) | (1ull << 7) | (1ull << 11) | (1ull << 13) | (1ull << 17) |
+    (1ull << 19) | (1ull << 23) | (1ull << 29) | (1ull << 31) | (1ull << 37) | (1ull << 41) |
+    (1ull << 43) | (1ull << 47) | (1ull << 53) | (1ull << 59) | (1ull << 61);
+
+// Marking-work partition (step A4): primes with at least kSmallHits hits per
+// segment are marked by residue class mod 32 (conflict-free atomics).
+constexpr uint32_t kSmallHits = 4096;
+// primes with fewer than kLaneHits hits per segment are marked lane-per-prime
+constexpr uint32_t kLaneHits = 64;
+
+// One work item of the batch kernel (step A10): one segment of one interval.
+struct BatchItem {
+  uint64_t a;         // first odd integer of the segment
+  uint32_t valid;     // odd slots in the segment (<= segment bits)
+  uint32_t interval;  // index of the interval (result slot)
+  uint32_t r;         // isqrt(hi_interval - 1): marking primes p <= r
+  uint32_t pad;
+};
+
+struct SieveParams {
+  uint64_t o0;        // lo | 1 : the odd integer of bit 0
+  uint64_t nbits;     // B = hi/2 - lo/2 odd slots
+  uint64_t nseg;      // segments (or batch items)
+  uint32_t seg_bits;  // S, a multiple of 1024
+  uint32_t r;         // marking primes p <= r
+  const uint32_t *primes;  // odd primes ascending (3, 5, 7, ...)
+  const uint64_t *recips;  // floor((2^64-1)/p)
+  const uint32_t *nbase;   // device count of primes[]
+  const uint32_t *tables;  // wheel tables, packed per group_offset()
+  uint32_t *out;           // bitmap mode: output words (bit 0 = word 0 bit 0)
+  uint64_t out_words;      // words of out
+  uint32_t out_vec4;       // out is 16-byte aligned
+  uint32_t add_two;        // 2 in [lo, hi): add (1, 2) to the result
+  uint32_t *seg_counts;    // optional per-segment prime counts (odd primes)
+  uint64_t *partials;      // [2 * gridDim.x]
+  unsigned int *done;      // last-block-done ticket (self-resetting)
+  uint64_t *result;        // [2] count, sum mod 2^64 (batch: [2 * nintervals])
+  const BatchItem *items;  // batch mode
+};
+
+enum Mode { kCount = 0, kBitmap = 1, kBatch = 2 };
+
+// launchers (kernels.cu)
+cudaError_t launch_sieve(int ng, int mode, const SieveParams &p, int grid, int threads,
+                         size_t smem, cudaStream_t s);
+cudaError_t set_sieve_smem_limits(size_t smem);
+cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64_t *recips,
+                               uint32_t cap, uint32_t *nbase, cudaStream_t s);
+cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
+                           uint32_t cap, cudaStream_t s);
+cudaError_t launch_scan_segments(const uint32_t *seg_counts, uint64_t nseg, uint64_t *seg_off,
+                                 uint32_t add_two, cudaStream_t s);
+cudaError_t launch_compact(const uint32_t *bitmap, uint64_t nbits, uint64_t o0, uint32_t seg_bits,
+                           uint64_t nseg, const uint64_t *seg_off, uint32_t add_two,
+                           uint64_t *out, uint64_t cap, cudaStream_t s);
+int sieve_max_ctas_per_sm(int ng, int mode, int threads, size_t smem);
+
+}  // namespace sv

@@ -1,0 +1,663 @@
+// kernels.cu -- the sm_100a kernels of the segmented sieve of Eratosthenes.
+//
+// Steps:
+//   A2  k_base_primes : odd primes <= r (one CTA, chunked shared-memory sieve)
+//   A3  wheel init    : segment <- OR of periodic composite patterns of 3..w
+//   A4  marking       : shared-memory atomicOr of the odd multiples of each
+//                       base prime w < p <= r, starting at max(p^2, first
+//                       odd multiple >= segment start)  (PAPER.md:131,
+//                       "iteratively marking as composite the multiples of
+//                       each prime"; SPEC.md:158 start rule)
+//   A5  large primes  : primes with < kLaneHits hits per segment are marked
+//                       lane-per-prime straight from their first hit, so a
+//                       segment a prime skips costs one Barrett reduction
+//   A6  count + sum   : popc of the inverted words, weighted popcs for the sum
+//   A7  bitmap        : 128-bit coalesced write-back of the inverted segment
+//   A8  list          : per-segment counts -> scan -> ballot/scan compaction
+//   A10 batch         : the same segment kernel over (interval, segment) items
+//
+// Bit j of a call's odd-only grid <-> the odd integer o0 + 2j (o0 = lo|1).
+// In shared memory a set bit means "composite" (the paper's marking); the
+// write-back inverts it so that the bitmap has 1 = prime (reading R5).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace sv {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mark(uint32_t *seg, uint32_t j) {
+  // bit j of the segment: word j>>5, bit j&31 (SHF.L.W wraps the shift)
+  atomicOr(&seg[j >> 5], __funnelshift_l(0u, 1u, j));
+}
+
+// Offset (in odd slots from a) of the first odd multiple m of p with
+// m >= max(a, p*p); kNone when p*p >= seg_end.  a is odd, m = a + 2*j.
+// a mod p by Barrett reduction with recip = floor((2^64-1)/p): the quotient
+// estimate is floor(a/p) or one less, so one conditional subtraction is exact
+// for any a < 2^64.
+__device__ __forceinline__ uint32_t first_hit(uint64_t a, uint64_t seg_end, uint32_t p,
+                                              uint64_t recip) {
+  const uint64_t pp = (uint64_t)p * p;
+  if (pp >= seg_end) return kNone;
+  const uint64_t q = __umul64hi(a, recip);
+  uint32_t r = (uint32_t)(a - q * (uint64_t)p);
+  if (r >= p) r -= p;
+  uint32_t d = r ? p - r : 0u;  // a + d == 0 (mod p)
+  if (d & 1u) d += p;           // a odd: the odd multiple is a + d with d even
+  uint32_t j = d >> 1;
+  if (a + 2ull * j < pp) j = (uint32_t)((pp - a) >> 1);
+  return j;
+}
+
+__device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t *v, uint32_t n, uint64_t x) {
+  uint32_t lo = 0, hi = n;  // first index with v[idx] > x
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if ((uint64_t)__ldg(v + mid) <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// sum of the bit indices of the set bits of w
+__device__ __forceinline__ uint32_t bit_index_sum(uint32_t w) {
+  return __popc(w & 0xAAAAAAAAu) + 2u * __popc(w & 0xCCCCCCCCu) + 4u * __popc(w & 0xF0F0F0F0u) +
+         8u * __popc(w & 0xFF00FF00u) + 16u * __popc(w & 0xFFFF0000u);
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Segment phases
+// ---------------------------------------------------------------------------
+
+// A3: wheel pre-sieve of one segment into seg (composite = 1), plus the
+// fix-ups (1 is not prime; wheel primes in range are prime) and the tail
+// (slots >= valid are set composite).  Thread t builds words t, t+nt, ...:
+// the 32 lanes of a warp read 32 consecutive table words (conflict-free) and
+// funnel-shift each window into place.  Words up to the end of the last quad
+// are written so that the epilogue can read whole uint4 quads.
+template <int NG>
+__device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, uint64_t o0,
+                                           uint64_t bit0, uint32_t valid, uint64_t a) {
+  const uint32_t nt = blockDim.x, tid = threadIdx.x;
+  const uint32_t nwords = ((valid + 127u) >> 7) << 2;
+  // table index of word w: ((o0-1)/2 + bit0 + 32*w) mod P_g
+  const uint64_t base = ((o0 - 1) >> 1) + bit0;
+  uint32_t ig[NG], dg[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const uint32_t P = group_period(g);
+    ig[g] = (uint32_t)((base % P + (uint64_t)(32u * tid) % P) % P);
+    dg[g] = (32u * nt) % P;
+  }
+  for (uint32_t w = tid; w < nwords; w += nt) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const uint32_t *t = tab + group_offset(g) + (ig[g] >> 5);
+      v |= __funnelshift_r(t[0], t[1], ig[g] & 31u);
+      ig[g] += dg[g];
+      if (ig[g] >= group_period(g)) ig[g] -= group_period(g);
+    }
+    const uint64_t n0 = a + 64ull * w;  // odd integer of the word's bit 0
+    if (n0 <= wheel_bound(NG)) {
+      for (uint32_t b = 0; b < 32u && n0 + 2ull * b <= wheel_bound(NG); ++b) {
+        const uint32_t n = (uint32_t)(n0 + 2ull * b);
+        if (n == 1u) v |= 1u << b;  // 1 is not prime (reading R2)
+        else if ((kOddPrimesBelow64 >> n) & 1ull) v &= ~(1u << b);
+      }
+    }
+    const int k = (int)valid - (int)(w << 5);  // valid slots in this word
+    if (k < 32) v = k <= 0 ? 0xFFFFFFFFu : (v | (0xFFFFFFFFu << k));
+    seg[w] = v;
+  }
+}
+
+struct PrimeRegions {
+  uint32_t start;  // first marking prime (after the wheel primes)
+  uint32_t mid;    // first prime with fewer than kSmallHits hits per full segment
+  uint32_t lanes;  // first prime with fewer than kLaneHits hits per full segment
+  uint32_t end;    // first prime > r
+};
+
+// A4/A5: mark the odd multiples of every base prime in [R.start, R.end).
+//
+// Three regions by hits per segment K ~ S/p:
+//  (i)  small primes (K >= kSmallHits): the hits k = r + 32m of residue class
+//       r (mod 32) all have the same bit (j0 + r p) & 31 and sit exactly p
+//       words apart, so lane l takes m = l + 32s: the 32 lanes of an atomic
+//       hit 32 distinct banks (p odd) with one warp-uniform mask, and a lane
+//       advances its byte address by 128 p per atomic (2 instructions/mark).
+//  (ii) medium primes: one prime per warp, lanes take consecutive hits.
+//  (iii) large primes (K < kLaneHits): one prime per lane.
+// First hits are computed 32 primes at a time (one Barrett reduction per
+// lane) and broadcast with shuffles.
+__device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__restrict__ primes,
+                                             const uint64_t *__restrict__ recips,
+                                             const PrimeRegions R, uint64_t a, uint32_t valid) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint64_t seg_end = a + 2ull * valid;
+  char *segb = reinterpret_cast<char *>(seg);
+  const uint32_t vw = valid >> 5, vb = valid & 31u;
+
+  // (i) small primes
+  for (uint32_t ib = R.start; ib < R.mid; ib += 32) {
+    const uint32_t i = ib + lane;
+    uint32_t pl = 0, jl = kNone;
+    if (i < R.mid) {
+      pl = __ldg(primes + i);
+      jl = first_hit(a, seg_end, pl, __ldg(recips + i));
+    }
+    const uint32_t nb = min(32u, R.mid - ib);
+    for (uint32_t k = 0; k < nb; ++k) {
+      const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
+      const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
+      if (j0 == kNone) break;  // p^2 past the segment, and so for every later prime
+      for (uint32_t r = warp; r < 32u; r += nw) {
+        const uint32_t jr = j0 + r * p;  // first hit of residue class r
+        if (jr >= valid) break;
+        const uint32_t bit = jr & 31u;
+        const uint32_t mask = 1u << bit;
+        const uint32_t alim = (vw + (bit < vb ? 1u : 0u)) << 2;
+        const uint32_t step = 128u * p;
+        uint32_t A = ((jr >> 5) + lane * p) << 2;
+        // byte offsets: 4 atomics per guard, then the remainder
+        for (; A + 3u * step < alim; A += 4u * step) {
+          atomicOr(reinterpret_cast<uint32_t *>(segb + A), mask);
+          atomicOr(reinterpret_cast<uint32_t *>(segb + A + step), mask);
+          atomicOr(reinterpret_cast<uint32_t *>(segb + A + 2u * step), mask);
+          atomicOr(reinterpret_cast<uint32_t *>(segb + A + 3u * step), mask);
+        }
+        for (; A < alim; A += step) atomicOr(reinterpret_cast<uint32_t *>(segb + A), mask);
+      }
+    }
+  }
+  // (ii) medium primes: prime i = R.mid + warp + nw*t, batches of 32 t's
+  for (uint32_t ib = R.mid + warp; ib < R.lanes; ib += 32u * nw) {
+    const uint32_t i = ib + lane * nw;
+    uint32_t pl = 0, jl = kNone;
+    if (i < R.lanes) {
+      pl = __ldg(primes + i);
+      jl = first_hit(a, seg_end, pl, __ldg(recips + i));
+    }
+    bool stop = false;
+    for (uint32_t k = 0; k < 32u; ++k) {
+      const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
+      const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
+      if (j0 == kNone) { stop = true; break; }
+      const uint32_t stride = 32u * p;
+      for (uint32_t j = j0 + lane * p; j < valid; j += stride) mark(seg, j);
+    }
+    if (stop) break;
+  }
+  // (iii) large primes: lane per prime (few hits each)
+  for (uint32_t k = R.lanes + threadIdx.x; k < R.end; k += blockDim.x) {
+    const uint32_t p = __ldg(primes + k);
+    const uint32_t j0 = first_hit(a, seg_end, p, __ldg(recips + k));
+    if (j0 == kNone) break;
+    for (uint32_t j = j0; j < valid; j += p) mark(seg, j);
+  }
+}
+
+// A6/A7: count, sum and (bitmap mode) write-back of one segment.
+template <int MODE>
+__device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t o0, uint64_t bit0,
+                                         uint32_t valid, uint32_t *out, uint64_t out_words,
+                                         uint32_t vec4, unsigned long long &cnt,
+                                         unsigned long long &sum) {
+  const uint32_t nq = (valid + 127u) >> 7;
+  const uint4 *seg4 = reinterpret_cast<const uint4 *>(seg);
+  const uint64_t w0 = bit0 >> 5;  // first word of the segment in the call's grid
+  for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+    const uint4 v = seg4[q];
+    const uint32_t w[4] = {~v.x, ~v.y, ~v.z, ~v.w};
+    const uint64_t gw = w0 + 4ull * q;
+    uint32_t c4 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = __popc(w[k]);
+      c4 += c;
+      // primes o0 + 64*(gw+k) + 2b for the set bits b
+      sum += (unsigned long long)c * (o0 + 64ull * (gw + k)) + 2ull * bit_index_sum(w[k]);
+    }
+    cnt += c4;
+    if (MODE == kBitmap) {
+      if (vec4 && gw + 4 <= out_words) {
+        reinterpret_cast<uint4 *>(out)[gw >> 2] = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (gw + k < out_words) out[gw + k] = w[k];
+      }
+    }
+  }
+}
+
+// block-wide sum of two u64 values; result valid in thread 0
+__device__ __forceinline__ void block_sum2(unsigned long long &x, unsigned long long &y,
+                                           unsigned long long *red) {
+  x = warp_sum_u64(x);
+  y = warp_sum_u64(y);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) { red[warp] = x; red[32 + warp] = y; }
+  __syncthreads();
+  if (warp == 0) {
+    x = lane < nw ? red[lane] : 0ull;
+    y = lane < nw ? red[32 + lane] : 0ull;
+    x = warp_sum_u64(x);
+    y = warp_sum_u64(y);
+  }
+}
+
+__device__ __forceinline__ void compute_regions(const SieveParams &P, PrimeRegions &R,
+                                                uint32_t ng_start) {
+  const uint32_t nb = *P.nbase;
+  R.end = upper_bound_u32(P.primes, nb, P.r);
+  R.start = min(ng_start, R.end);
+  // primes with >= kSmallHits hits in a full segment: p * kSmallHits <= S
+  R.mid = max(R.start, min(R.end, upper_bound_u32(P.primes, nb, P.seg_bits / kSmallHits)));
+  R.lanes = max(R.mid, min(R.end, upper_bound_u32(P.primes, nb, P.seg_bits / kLaneHits)));
+}
+
+// ---------------------------------------------------------------------------
+// The segmented sieve kernel.  Persistent CTAs walk the segments round robin;
+// each segment lives in shared memory for its whole life (init -> mark ->
+// count/write-back), so nothing but the bitmap (bitmap mode) and 16 bytes per
+// CTA ever reach HBM.
+// ---------------------------------------------------------------------------
+template <int NG, int MODE>
+__global__ void __launch_bounds__(1024, 1) k_sieve(const SieveParams P) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  uint32_t *seg = smem;
+  uint32_t *tab = smem + P.seg_bits / 32;
+  __shared__ unsigned long long red[64];
+  __shared__ PrimeRegions sR;
+  __shared__ uint32_t s_last;
+
+  for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
+  if (threadIdx.x == 0 && MODE != kBatch) compute_regions(P, sR, wheel_nprimes(NG));
+  __syncthreads();
+
+  unsigned long long cnt = 0, sum = 0;
+  for (uint64_t s = blockIdx.x; s < P.nseg; s += gridDim.x) {
+    uint64_t a, bit0, o0;
+    uint32_t valid;
+    if (MODE == kBatch) {
+      const BatchItem it = P.items[s];
+      a = it.a; valid = it.valid; o0 = it.a; bit0 = 0;
+      if (threadIdx.x == 0) {
+        SieveParams Q = P;
+        Q.r = it.r;
+        compute_regions(Q, sR, wheel_nprimes(NG));
+      }
+    } else {
+      o0 = P.o0;
+      bit0 = s * (uint64_t)P.seg_bits;
+      const uint64_t left = P.nbits - bit0;
+      valid = left < P.seg_bits ? (uint32_t)left : P.seg_bits;
+      a = o0 + 2ull * bit0;
+    }
+    wheel_init<NG>(seg, tab, o0, bit0, valid, a);
+    __syncthreads();
+    mark_segment(seg, P.primes, P.recips, sR, a, valid);
+    __syncthreads();
+    if (MODE == kBatch) {
+      unsigned long long c = 0, sm = 0;
+      epilogue<kCount>(seg, o0, bit0, valid, nullptr, 0, 0, c, sm);
+      block_sum2(c, sm, red);
+      if (threadIdx.x == 0) {
+        const uint32_t iv = P.items[s].interval;
+        atomicAdd(reinterpret_cast<unsigned long long *>(P.result) + 2 * iv, c);
+        atomicAdd(reinterpret_cast<unsigned long long *>(P.result) + 2 * iv + 1, sm);
+      }
+      __syncthreads();
+    } else if (MODE == kBitmap && P.seg_counts) {
+      unsigned long long c = 0, sm = 0;
+      epilogue<kBitmap>(seg, o0, bit0, valid, P.out, P.out_words, P.out_vec4, c, sm);
+      cnt += c;
+      sum += sm;
+      unsigned long long c2 = c, z = 0;
+      block_sum2(c2, z, red);
+      if (threadIdx.x == 0) P.seg_counts[s] = (uint32_t)c2;
+      __syncthreads();
+    } else {
+      epilogue<MODE>(seg, o0, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
+      __syncthreads();
+    }
+  }
+  if (MODE == kBatch) return;
+
+  // per-CTA partial, then the last CTA to finish reduces all partials in a
+  // fixed order (deterministic) and writes the result.
+  block_sum2(cnt, sum, red);
+  if (threadIdx.x == 0) {
+    P.partials[2 * blockIdx.x] = cnt;
+    P.partials[2 * blockIdx.x + 1] = sum;
+    __threadfence();
+    const unsigned int t = atomicAdd(P.done, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    unsigned long long c = 0, sm = 0;
+    for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+      c += __ldcg(reinterpret_cast<const unsigned long long *>(P.partials) + 2 * b);
+      sm += __ldcg(reinterpret_cast<const unsigned long long *>(P.partials) + 2 * b + 1);
+    }
+    block_sum2(c, sm, red);
+    if (threadIdx.x == 0) {
+      if (P.add_two) { c += 1; sm += 2; }
+      P.result[0] = c;
+      P.result[1] = sm;
+      *P.done = 0u;  // ready for the next launch
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// A2: base primes.  One CTA: odd primes <= rs = isqrt(r) by trial division,
+// then the odd numbers <= r are sieved in shared-memory chunks and compacted
+// in order (block scan of per-thread counts).  Also writes the Barrett
+// reciprocal of every prime.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kBaseChunkBits = 1u << 19;  // 64 KiB of shared memory
+constexpr uint32_t kMaxSmall = 1024;           // odd primes <= 4096 number 563
+
+__global__ void __launch_bounds__(1024, 1) k_base_primes(uint32_t r, uint32_t rs, uint32_t *primes,
+                                                         uint64_t *recips, uint32_t cap,
+                                                         uint32_t *nbase) {
+  extern __shared__ __align__(16) uint32_t bm[];  // kBaseChunkBits / 32 words
+  __shared__ uint32_t sp[kMaxSmall];
+  __shared__ uint32_t s_wsum[32];
+  __shared__ uint32_t s_nsp, s_total;
+  const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t nw = nt >> 5;
+  if (tid == 0) { s_nsp = 0; s_total = 0; }
+  __syncthreads();
+
+  // small odd primes q <= rs, in ascending order: rounds of nt candidates
+  for (uint32_t base = 3; base <= rs; base += 2 * nt) {
+    const uint32_t q = base + 2 * tid;
+    bool isp = q <= rs;
+    for (uint32_t d = 3; isp && d * d <= q; d += 2)
+      if (q % d == 0) isp = false;
+    const uint32_t bal = __ballot_sync(0xffffffffu, isp);
+    if (lane == 0) s_wsum[warp] = __popc(bal);
+    __syncthreads();
+    uint32_t off = s_nsp;
+    for (uint32_t w = 0; w < warp; ++w) off += s_wsum[w];
+    off += __popc(bal & ((1u << lane) - 1u));
+    if (isp && off < kMaxSmall) sp[off] = q;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t t = 0;
+      for (uint32_t w = 0; w < nw; ++w) t += s_wsum[w];
+      s_nsp += t;
+    }
+    __syncthreads();
+  }
+  const uint32_t nsp = min(s_nsp, kMaxSmall);
+
+  // odd n = 2i+1 for i in [1, imax]; chunk [i0, i0 + kBaseChunkBits)
+  const uint32_t imax = r >= 3 ? (r - 1) / 2 : 0;
+  for (uint32_t i0 = 1; i0 <= imax; i0 += kBaseChunkBits) {
+    const uint32_t nbits = min(kBaseChunkBits, imax - i0 + 1);
+    const uint32_t nwords = (nbits + 31) / 32;
+    for (uint32_t w = tid; w < nwords; w += nt) bm[w] = 0;
+    __syncthreads();
+    const uint64_t a = 2ull * i0 + 1;  // odd integer of bit 0
+    const uint64_t e = a + 2ull * nbits;
+    for (uint32_t k = warp; k < nsp; k += nw) {
+      const uint32_t q = sp[k];
+      const uint64_t qq = (uint64_t)q * q;
+      if (qq >= e) break;
+      uint64_t m = qq;
+      if (m < a) {
+        m = ((a + q - 1) / q) * q;
+        if (!(m & 1ull)) m += q;
+      }
+      for (uint64_t j = (m - a) / 2 + (uint64_t)lane * q; j < nbits; j += 32ull * q)
+        atomicOr(&bm[j >> 5], 1u << (j & 31));
+    }
+    __syncthreads();
+    // compaction: thread t owns words [t*wpt, (t+1)*wpt)
+    const uint32_t wpt = (nwords + nt - 1) / nt;
+    const uint32_t wb = tid * wpt, we = min(nwords, wb + wpt);
+    uint32_t c = 0;
+    for (uint32_t w = wb; w < we; ++w) {
+      uint32_t x = ~bm[w];
+      if (w == nwords - 1 && (nbits & 31)) x &= (1u << (nbits & 31)) - 1u;
+      c += __popc(x);
+    }
+    // block exclusive scan of c
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    uint32_t off = s_total + incl - c;
+    for (uint32_t w = 0; w < warp; ++w) off += s_wsum[w];
+    for (uint32_t w = wb; w < we; ++w) {
+      uint32_t x = ~bm[w];
+      if (w == nwords - 1 && (nbits & 31)) x &= (1u << (nbits & 31)) - 1u;
+      while (x) {
+        const uint32_t b = __ffs(x) - 1;
+        x &= x - 1;
+        const uint32_t p = (uint32_t)(a + 2ull * (32ull * w + b));
+        if (off < cap) {
+          primes[off] = p;
+          recips[off] = ~0ull / p;
+        }
+        ++off;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t t = 0;
+      for (uint32_t w = 0; w < nw; ++w) t += s_wsum[w];
+      s_total += t;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *nbase = min(s_total, cap);
+}
+
+__global__ void k_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
+                          uint32_t cap) {
+  const uint32_t n = min(*nbase, cap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    recips[i] = ~0ull / primes[i];
+}
+
+// ---------------------------------------------------------------------------
+// A8: list compaction.  seg_off[s] = exclusive prefix of seg_counts (+1 when
+// 2 is in range, which takes list slot 0).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_scan_segments(const uint32_t *seg_counts, uint64_t nseg,
+                                                        uint64_t *seg_off, uint32_t add_two) {
+  __shared__ unsigned long long s_w[32];
+  __shared__ unsigned long long s_carry;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) s_carry = add_two;
+  __syncthreads();
+  for (uint64_t base = 0; base < nseg; base += blockDim.x) {
+    const uint64_t i = base + tid;
+    const unsigned long long v = i < nseg ? seg_counts[i] : 0ull;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    unsigned long long off = s_carry + incl - v;
+    for (uint32_t w = 0; w < warp; ++w) off += s_w[w];
+    if (i < nseg) seg_off[i] = off;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t = 0;
+      for (uint32_t w = 0; w < nw; ++w) t += s_w[w];
+      s_carry += t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_compact(const uint32_t *__restrict__ bitmap, uint64_t nbits,
+                                                  uint64_t o0, uint32_t seg_bits, uint64_t nseg,
+                                                  const uint64_t *__restrict__ seg_off,
+                                                  uint32_t add_two, uint64_t *__restrict__ out,
+                                                  uint64_t cap) {
+  __shared__ uint32_t s_w[32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (add_two && blockIdx.x == 0 && tid == 0 && cap > 0) out[0] = 2;
+  const uint64_t words = (nbits + 31) / 32;
+  const uint32_t seg_words = seg_bits / 32;
+  for (uint64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+    uint64_t off = seg_off[s];
+    if (off >= cap) continue;  // everything here lands past the cap
+    const uint64_t wb = s * seg_words;
+    const uint64_t we = min(words, wb + seg_words);
+    for (uint64_t w0 = wb; w0 < we; w0 += blockDim.x) {
+      const uint64_t w = w0 + tid;
+      const uint32_t x = w < we ? __ldg(bitmap + w) : 0u;
+      const uint32_t c = __popc(x);
+      const uint32_t bal_incl = c;
+      uint32_t incl = bal_incl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      if (lane == 31) s_w[warp] = incl;
+      __syncthreads();
+      uint64_t my = off + incl - c;
+      uint32_t tot = 0;
+      for (uint32_t k = 0; k < nw; ++k) {
+        if (k < warp) my += s_w[k];
+        tot += s_w[k];
+      }
+      uint32_t y = x;
+      while (y) {
+        const uint32_t b = __ffs(y) - 1;
+        y &= y - 1;
+        if (my < cap) out[my] = o0 + 2ull * (32ull * w + b);
+        ++my;
+      }
+      off += tot;
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+template <int NG, int MODE>
+static cudaError_t launch_t(const SieveParams &p, int grid, int threads, size_t smem, cudaStream_t s) {
+  k_sieve<NG, MODE><<<grid, threads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_m(int ng, const SieveParams &p, int grid, int threads, size_t smem,
+                            cudaStream_t s) {
+  switch (ng) {
+    case 2: return launch_t<2, MODE>(p, grid, threads, smem, s);
+    case 3: return launch_t<3, MODE>(p, grid, threads, smem, s);
+    case 4: return launch_t<4, MODE>(p, grid, threads, smem, s);
+    case 5: return launch_t<5, MODE>(p, grid, threads, smem, s);
+    case 6: return launch_t<6, MODE>(p, grid, threads, smem, s);
+    case 7: return launch_t<7, MODE>(p, grid, threads, smem, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_sieve(int ng, int mode, const SieveParams &p, int grid, int threads, size_t smem,
+                         cudaStream_t s) {
+  switch (mode) {
+    case kCount: return launch_m<kCount>(ng, p, grid, threads, smem, s);
+    case kBitmap: return launch_m<kBitmap>(ng, p, grid, threads, smem, s);
+    case kBatch: return launch_m<kBatch>(ng, p, grid, threads, smem, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int NG>
+static cudaError_t set_attr_ng(size_t smem) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_sieve<NG, kCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  if ((e = cudaFuncSetAttribute(k_sieve<NG, kBitmap>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  return cudaFuncSetAttribute(k_sieve<NG, kBatch>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t set_sieve_smem_limits(size_t smem) {
+  cudaError_t e;
+  if ((e = set_attr_ng<2>(smem))) return e;
+  if ((e = set_attr_ng<3>(smem))) return e;
+  if ((e = set_attr_ng<4>(smem))) return e;
+  if ((e = set_attr_ng<5>(smem))) return e;
+  if ((e = set_attr_ng<6>(smem))) return e;
+  if ((e = set_attr_ng<7>(smem))) return e;
+  return cudaFuncSetAttribute(k_base_primes, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(kBaseChunkBits / 8));
+}
+
+template <int NG, int MODE>
+static int occ_t(int threads, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sieve<NG, MODE>, threads, smem) != cudaSuccess)
+    return 0;
+  return n;
+}
+
+int sieve_max_ctas_per_sm(int ng, int mode, int threads, size_t smem) {
+  (void)ng; (void)mode;
+  return occ_t<5, kCount>(threads, smem);
+}
+
+cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64_t *recips,
+                               uint32_t cap, uint32_t *nbase, cudaStream_t s) {
+  k_base_primes<<<1, 1024, kBaseChunkBits / 8, s>>>(r, rs, primes, recips, cap, nbase);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
+                           uint32_t cap, cudaStream_t s) {
+  const int grid = (int)((cap + 255) / 256 < 1184 ? (cap + 255) / 256 : 1184);
+  k_prepare<<<grid > 0 ? grid : 1, 256, 0, s>>>(primes, nbase, recips, cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan_segments(const uint32_t *seg_counts, uint64_t nseg, uint64_t *seg_off,
+                                 uint32_t add_two, cudaStream_t s) {
+  k_scan_segments<<<1, 1024, 0, s>>>(seg_counts, nseg, seg_off, add_two);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const uint32_t *bitmap, uint64_t nbits, uint64_t o0, uint32_t seg_bits,
+                           uint64_t nseg, const uint64_t *seg_off, uint32_t add_two, uint64_t *out,
+                           uint64_t cap, cudaStream_t s) {
+  int grid = nseg < 148 * 8 ? (int)nseg : 148 * 8;
+  if (grid < 1) grid = 1;
+  k_compact<<<grid, 1024, 0, s>>>(bitmap, nbits, o0, seg_bits, nseg, seg_off, add_two, out, cap);
+  return cudaGetLastError();
+}
+
+}  // namespace sv

@@ -1,0 +1,636 @@
+// runtime.cu -- host runtime and C ABI of libsieve.so (include/sieve.h).
+//
+// Responsibilities: argument validation (error codes of sieve.h), planning of
+// a call (step A1: odd-only grid, segments, grid size), device scratch owned
+// by the library, stream handling, host<->device staging for host outputs,
+// and the launch sequences of the three north_star calls:
+//   count  : K1 base primes -> sieve(count) [last CTA reduces]     2 launches
+//   bitmap : K1 -> sieve(bitmap, 128-bit write-back)                2 launches
+//   primes : K1 -> sieve(bitmap->scratch, seg counts) -> scan -> compact
+// No C++ exception crosses the ABI; there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sieve.h"
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? SIEVE_ENOMEM : SIEVE_ECUDA,          \
+                  "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define TRY(expr)           \
+  do {                      \
+    int rc_ = (expr);       \
+    if (rc_ < 0) return rc_; \
+  } while (0)
+
+// exact integer square root (largest r with r*r <= x), x < 2^64
+uint64_t isqrt_u64(uint64_t x) {
+  uint64_t r = (uint64_t)std::sqrt((double)x);
+  while (r > 0 && r * r > x) --r;
+  while ((r + 1) * (r + 1) <= x) ++r;
+  return r;
+}
+
+struct Plan {           // step A1 for one range [lo, hi)
+  uint64_t lo = 0, hi = 0;
+  uint64_t o0 = 1;      // lo | 1
+  uint64_t nbits = 0;   // odd slots B
+  uint64_t words = 0;   // ceil(B/32)
+  uint64_t nseg = 0;    // ceil(B/S)
+  uint64_t r = 0;       // isqrt(hi-1)
+  bool two = false;     // 2 in [lo, hi)
+};
+
+template <typename T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  int ensure(size_t need) {
+    if (need <= n) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t want = std::max(need, n + n / 2);
+    cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+    if (e != cudaSuccess) {
+      e = cudaMalloc(&p, need * sizeof(T));
+      if (e != cudaSuccess) {
+        p = nullptr;
+        return fail(SIEVE_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", need * sizeof(T),
+                    cudaGetErrorString(e));
+      }
+      want = need;
+    }
+    n = want;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct Ctx {
+  std::mutex mu;
+  int device = -1;
+  bool ready = false;
+  int nsm = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t user = nullptr;
+  bool user_set = false;
+  sieve_options opt{};
+  size_t smem_limit_set = 0;
+  DevBuf<uint32_t> tables;
+  DevBuf<uint32_t> primes;
+  DevBuf<uint64_t> recips;
+  DevBuf<uint32_t> nbase;
+  DevBuf<uint64_t> partials;
+  DevBuf<unsigned int> done;
+  DevBuf<uint64_t> result;
+  DevBuf<uint32_t> bitmap;
+  DevBuf<uint32_t> segcnt;
+  DevBuf<uint64_t> segoff;
+  DevBuf<uint64_t> list;
+  DevBuf<sv::BatchItem> items;
+  DevBuf<uint64_t> bres;
+  uint64_t *h_res = nullptr;  // pinned [2]
+  cudaStream_t stream() const { return user_set ? user : own; }
+};
+
+Ctx g;
+
+void default_options(sieve_options &o) {
+  memset(&o, 0, sizeof o);
+  o.segment_kb = 192;
+  o.wheel = 37;
+  o.ctas_per_sm = 0;
+  o.threads = 1024;
+}
+
+int ng_for_wheel(uint32_t w) {
+  switch (w) {
+    case 19: return 2;
+    case 29: return 3;
+    case 37: return 4;
+    case 43: return 5;
+    case 53: return 6;
+    case 61: return 7;
+    default: return -1;
+  }
+}
+
+// wheel table g: bit i set iff 2i+1 is divisible by a prime of group g
+void build_tables(std::vector<uint32_t> &t) {
+  static const uint32_t groups[sv::kMaxGroups][5] = {
+      {3, 5, 7, 11, 13}, {17, 19, 0, 0, 0}, {23, 29, 0, 0, 0}, {31, 37, 0, 0, 0},
+      {41, 43, 0, 0, 0}, {47, 53, 0, 0, 0}, {59, 61, 0, 0, 0}};
+  t.assign(sv::tables_words(sv::kMaxGroups), 0u);
+  for (int g = 0; g < sv::kMaxGroups; ++g) {
+    const uint32_t nbits = sv::group_words(g) * 32;
+    uint32_t *w = t.data() + sv::group_offset(g);
+    for (uint32_t i = 0; i < nbits; ++i) {
+      const uint64_t n = 2ull * i + 1;
+      bool hit = false;
+      for (int k = 0; k < 5 && groups[g][k]; ++k) hit |= (n % groups[g][k]) == 0;
+      if (hit) w[i >> 5] |= 1u << (i & 31);
+    }
+  }
+}
+
+int ensure_ready() {
+  if (g.ready) return 0;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev <= 0)
+    return fail(SIEVE_ENODEV, "no CUDA device available (%s)", cudaGetErrorString(e));
+  if (g.device < 0) CUDA_TRY(cudaGetDevice(&g.device));
+  CUDA_TRY(cudaSetDevice(g.device));
+  CUDA_TRY(cudaDeviceGetAttribute(&g.nsm, cudaDevAttrMultiProcessorCount, g.device));
+  if (!g.own) CUDA_TRY(cudaStreamCreateWithFlags(&g.own, cudaStreamNonBlocking));
+  if (g.opt.segment_kb == 0) default_options(g.opt);
+  std::vector<uint32_t> t;
+  build_tables(t);
+  TRY(g.tables.ensure(t.size()));
+  CUDA_TRY(cudaMemcpy(g.tables.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+  TRY(g.done.ensure(1));
+  CUDA_TRY(cudaMemset(g.done.p, 0, sizeof(unsigned int)));
+  TRY(g.result.ensure(2));
+  if (!g.h_res) CUDA_TRY(cudaMallocHost(&g.h_res, 2 * sizeof(uint64_t)));
+  g.ready = true;
+  return 0;
+}
+
+size_t seg_bits() { return (size_t)g.opt.segment_kb * 8192; }
+size_t sieve_smem() { return seg_bits() / 8 + sv::tables_words(sv::kMaxGroups) * 4; }
+
+int ensure_smem_attr() {
+  const size_t sm = sieve_smem();
+  if (g.smem_limit_set == sm) return 0;
+  CUDA_TRY(sv::set_sieve_smem_limits(sm));
+  g.smem_limit_set = sm;
+  return 0;
+}
+
+int grid_for(uint64_t nseg) {
+  int per = g.opt.ctas_per_sm;
+  if (per <= 0) {
+    per = sv::sieve_max_ctas_per_sm(0, 0, (int)g.opt.threads, sieve_smem());
+    if (per <= 0) per = 1;
+  }
+  uint64_t grid = (uint64_t)g.nsm * per;
+  if (grid > nseg) grid = nseg;
+  return grid < 1 ? 1 : (int)grid;
+}
+
+int validate(uint64_t lo, uint64_t hi) {
+  if (lo > hi) return fail(SIEVE_EINVAL, "lo (%llu) > hi (%llu)", (unsigned long long)lo,
+                           (unsigned long long)hi);
+  if (hi > SIEVE_MAX_HI) return fail(SIEVE_ERANGE, "hi (%llu) > 2^48", (unsigned long long)hi);
+  return 0;
+}
+
+Plan make_plan(uint64_t lo, uint64_t hi) {
+  Plan P;
+  P.lo = lo;
+  P.hi = hi;
+  P.o0 = lo | 1;
+  P.nbits = hi > lo ? hi / 2 - lo / 2 : 0;
+  P.words = (P.nbits + 31) / 32;
+  P.nseg = (P.nbits + seg_bits() - 1) / seg_bits();
+  P.r = hi >= 2 ? isqrt_u64(hi - 1) : 0;
+  P.two = lo <= 2 && 2 < hi;
+  return P;
+}
+
+int ensure_smem_attr();
+
+uint64_t base_capacity(uint64_t r) {
+  // pi(x) < 1.25506 x / ln x for x > 1 (Rosser-Schoenfeld); generous slack
+  if (r < 64) return 32;
+  const double x = (double)r;
+  return (uint64_t)(1.26 * x / std::log(x)) + 64;
+}
+
+// K1 into the library's scratch (or the given buffers)
+int base_primes(uint64_t r, uint32_t *primes, uint64_t *recips, uint64_t cap, uint32_t *nbase,
+                cudaStream_t s) {
+  if (r > (1ull << 24)) return fail(SIEVE_ERANGE, "base-prime bound %llu > 2^24", (unsigned long long)r);
+  const uint32_t rs = (uint32_t)isqrt_u64(r);
+  TRY(ensure_smem_attr());
+  CUDA_TRY(sv::launch_base_primes((uint32_t)r, rs, primes, recips, (uint32_t)cap, nbase, s));
+  g_launches += 1;
+  return 0;
+}
+
+int own_base(uint64_t r) {
+  const uint64_t cap = base_capacity(r);
+  TRY(g.primes.ensure(cap));
+  TRY(g.recips.ensure(cap));
+  TRY(g.nbase.ensure(1));
+  return base_primes(r, g.primes.p, g.recips.p, cap, g.nbase.p, g.stream());
+}
+
+sv::SieveParams params_for(const Plan &P, const uint32_t *primes, const uint64_t *recips,
+                           const uint32_t *nbase, uint64_t *result) {
+  sv::SieveParams sp;
+  memset(&sp, 0, sizeof sp);
+  sp.o0 = P.o0;
+  sp.nbits = P.nbits;
+  sp.nseg = P.nseg;
+  sp.seg_bits = (uint32_t)seg_bits();
+  sp.r = (uint32_t)P.r;
+  sp.primes = primes;
+  sp.recips = recips;
+  sp.nbase = nbase;
+  sp.tables = g.tables.p;
+  sp.add_two = P.two ? 1u : 0u;
+  sp.done = g.done.p;
+  sp.result = result;
+  return sp;
+}
+
+int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork) {
+  TRY(ensure_smem_attr());
+  const int grid = grid_for(nwork);
+  TRY(g.partials.ensure(2 * (size_t)grid));
+  sp.partials = g.partials.p;
+  const int ng = ng_for_wheel(g.opt.wheel);
+  CUDA_TRY(sv::launch_sieve(ng, mode, sp, grid, (int)g.opt.threads, sieve_smem(), g.stream()));
+  g_launches += 1;
+  return 0;
+}
+
+// count/sum of [lo, hi) into device result[0..1]; empty/odd-free ranges handled
+int stats_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase,
+                uint64_t *result) {
+  if (P.nbits == 0) {
+    uint64_t h[2] = {P.two ? 1ull : 0ull, P.two ? 2ull : 0ull};
+    CUDA_TRY(cudaMemcpyAsync(result, h, sizeof h, cudaMemcpyHostToDevice, g.stream()));
+    CUDA_TRY(cudaStreamSynchronize(g.stream()));  // h is on this stack frame
+    return 0;
+  }
+  sv::SieveParams sp = params_for(P, primes, recips, nbase, result);
+  return run_sieve(sv::kCount, sp, P.nseg);
+}
+
+int bitmap_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase,
+                 uint32_t *out, uint32_t *segcnt, uint64_t *result) {
+  if (P.nbits == 0) return stats_async(P, primes, recips, nbase, result);
+  sv::SieveParams sp = params_for(P, primes, recips, nbase, result);
+  sp.out = out;
+  sp.out_words = P.words;
+  sp.out_vec4 = ((uintptr_t)out & 15u) == 0 ? 1u : 0u;
+  sp.seg_counts = segcnt;
+  return run_sieve(sv::kBitmap, sp, P.nseg);
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int fetch_result(uint64_t *count, uint64_t *sum) {
+  CUDA_TRY(cudaMemcpyAsync(g.h_res, g.result.p, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                           g.stream()));
+  CUDA_TRY(cudaStreamSynchronize(g.stream()));
+  if (count) *count = g.h_res[0];
+  if (sum) *sum = g.h_res[1];
+  return 0;
+}
+
+int do_stats(uint64_t lo, uint64_t hi, uint64_t *count, uint64_t *sum) {
+  TRY(validate(lo, hi));
+  TRY(ensure_ready());
+  const Plan P = make_plan(lo, hi);
+  if (P.nbits == 0) {
+    if (count) *count = P.two ? 1 : 0;
+    if (sum) *sum = P.two ? 2 : 0;
+    return 0;
+  }
+  TRY(own_base(P.r));
+  TRY(stats_async(P, g.primes.p, g.recips.p, g.nbase.p, g.result.p));
+  return fetch_result(count, sum);
+}
+
+int64_t do_bitmap(uint64_t lo, uint64_t hi, uint32_t *out) {
+  TRY(validate(lo, hi));
+  const Plan P0 = make_plan(lo, hi);
+  if (P0.words > 0 && !out) return fail(SIEVE_EINVAL, "out is NULL for %llu words", (unsigned long long)P0.words);
+  TRY(ensure_ready());
+  const Plan P = make_plan(lo, hi);
+  if (P.nbits == 0) return P.two ? 1 : 0;
+  TRY(own_base(P.r));
+  const bool dev = is_device_ptr(out);
+  uint32_t *dst = out;
+  if (!dev) {
+    TRY(g.bitmap.ensure(P.words));
+    dst = g.bitmap.p;
+  }
+  TRY(bitmap_async(P, g.primes.p, g.recips.p, g.nbase.p, dst, nullptr, g.result.p));
+  if (!dev)
+    CUDA_TRY(cudaMemcpyAsync(out, dst, P.words * 4, cudaMemcpyDeviceToHost, g.stream()));
+  uint64_t c = 0;
+  TRY(fetch_result(&c, nullptr));
+  return (int64_t)c;
+}
+
+int64_t do_primes(uint64_t lo, uint64_t hi, uint64_t *out, uint64_t cap) {
+  TRY(validate(lo, hi));
+  if (cap > 0 && !out) return fail(SIEVE_EINVAL, "out is NULL with cap %llu", (unsigned long long)cap);
+  TRY(ensure_ready());
+  const Plan P = make_plan(lo, hi);
+  if (P.nbits == 0) {
+    if (P.two && cap > 0) {
+      const uint64_t two = 2;
+      if (is_device_ptr(out)) {
+        CUDA_TRY(cudaMemcpyAsync(out, &two, 8, cudaMemcpyHostToDevice, g.stream()));
+        CUDA_TRY(cudaStreamSynchronize(g.stream()));
+      } else {
+        out[0] = 2;
+      }
+    }
+    return P.two ? 1 : 0;
+  }
+  TRY(own_base(P.r));
+  TRY(g.bitmap.ensure(P.words + 4));
+  TRY(g.segcnt.ensure(P.nseg));
+  TRY(bitmap_async(P, g.primes.p, g.recips.p, g.nbase.p, g.bitmap.p, g.segcnt.p, g.result.p));
+  if (cap > 0) {
+    TRY(g.segoff.ensure(P.nseg));
+    CUDA_TRY(sv::launch_scan_segments(g.segcnt.p, P.nseg, g.segoff.p, P.two ? 1u : 0u, g.stream()));
+    g_launches += 1;
+    const bool dev = is_device_ptr(out);
+    uint64_t *dst = out;
+    if (!dev) {
+      TRY(g.list.ensure(cap));
+      dst = g.list.p;
+    }
+    CUDA_TRY(sv::launch_compact(g.bitmap.p, P.nbits, P.o0, (uint32_t)seg_bits(), P.nseg, g.segoff.p,
+                                P.two ? 1u : 0u, dst, cap, g.stream()));
+    g_launches += 1;
+    uint64_t c = 0;
+    TRY(fetch_result(&c, nullptr));
+    if (!dev) {
+      const uint64_t n = std::min(c, cap);
+      CUDA_TRY(cudaMemcpyAsync(out, dst, n * 8, cudaMemcpyDeviceToHost, g.stream()));
+      CUDA_TRY(cudaStreamSynchronize(g.stream()));
+    }
+    return (int64_t)c;
+  }
+  uint64_t c = 0;
+  TRY(fetch_result(&c, nullptr));
+  return (int64_t)c;
+}
+
+int do_batch(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t *count, uint64_t *sum) {
+  if (n == 0) return 0;
+  if (!lo || !hi || !count || !sum) return fail(SIEVE_EINVAL, "NULL array in sieve_batch");
+  uint64_t maxhi = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    TRY(validate(lo[i], hi[i]));
+    maxhi = std::max(maxhi, hi[i]);
+  }
+  TRY(ensure_ready());
+  // step A10 plan: one item per (interval, segment)
+  const uint64_t S = seg_bits();
+  std::vector<sv::BatchItem> items;
+  for (uint64_t i = 0; i < n; ++i) {
+    const Plan P = make_plan(lo[i], hi[i]);
+    for (uint64_t b = 0; b < P.nbits; b += S) {
+      sv::BatchItem it;
+      it.a = P.o0 + 2 * b;
+      it.valid = (uint32_t)std::min<uint64_t>(S, P.nbits - b);
+      it.interval = (uint32_t)i;
+      it.r = (uint32_t)P.r;
+      it.pad = 0;
+      items.push_back(it);
+    }
+  }
+  const uint64_t rmax = maxhi >= 2 ? isqrt_u64(maxhi - 1) : 0;
+  TRY(own_base(rmax));
+  TRY(g.bres.ensure(2 * n));
+  CUDA_TRY(cudaMemsetAsync(g.bres.p, 0, 2 * n * sizeof(uint64_t), g.stream()));
+  if (!items.empty()) {
+    TRY(g.items.ensure(items.size()));
+    CUDA_TRY(cudaMemcpyAsync(g.items.p, items.data(), items.size() * sizeof(sv::BatchItem),
+                             cudaMemcpyHostToDevice, g.stream()));
+    Plan dummy = make_plan(0, 0);
+    sv::SieveParams sp = params_for(dummy, g.primes.p, g.recips.p, g.nbase.p, g.bres.p);
+    sp.items = g.items.p;
+    sp.nseg = items.size();
+    sp.r = (uint32_t)rmax;
+    TRY(run_sieve(sv::kBatch, sp, items.size()));
+  }
+  std::vector<uint64_t> h(2 * n);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), g.bres.p, 2 * n * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                           g.stream()));
+  CUDA_TRY(cudaStreamSynchronize(g.stream()));
+  for (uint64_t i = 0; i < n; ++i) {
+    const bool two = lo[i] <= 2 && 2 < hi[i];
+    count[i] = h[2 * i] + (two ? 1 : 0);
+    sum[i] = h[2 * i + 1] + (two ? 2 : 0);
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int64_t sieve_count(uint64_t lo, uint64_t hi) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  uint64_t c = 0;
+  TRY(do_stats(lo, hi, &c, nullptr));
+  return (int64_t)c;
+}
+
+int64_t sieve_bitmap(uint64_t lo, uint64_t hi, uint32_t *out) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  return do_bitmap(lo, hi, out);
+}
+
+int64_t sieve_primes(uint64_t lo, uint64_t hi, uint64_t *out, uint64_t cap) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  return do_primes(lo, hi, out, cap);
+}
+
+uint64_t sieve_bitmap_words(uint64_t lo, uint64_t hi) {
+  if (hi <= lo) return 0;
+  return (hi / 2 - lo / 2 + 31) / 32;
+}
+
+int sieve_stats(uint64_t lo, uint64_t hi, uint64_t *count, uint64_t *sum_mod_2_64) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!count || !sum_mod_2_64) return fail(SIEVE_EINVAL, "NULL output in sieve_stats");
+  return do_stats(lo, hi, count, sum_mod_2_64);
+}
+
+int sieve_batch(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t *count,
+                uint64_t *sum_mod_2_64) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  return do_batch(lo, hi, n, count, sum_mod_2_64);
+}
+
+uint64_t sieve_base_capacity(uint64_t r) { return base_capacity(r); }
+
+int sieve_base_primes_async(uint64_t r, uint32_t *primes, uint64_t *recips, uint64_t cap,
+                            uint32_t *nbase) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!primes || !recips || !nbase) return fail(SIEVE_EINVAL, "NULL buffer");
+  if (cap < base_capacity(r)) return fail(SIEVE_EINVAL, "cap %llu < sieve_base_capacity(%llu)",
+                                          (unsigned long long)cap, (unsigned long long)r);
+  TRY(ensure_ready());
+  return base_primes(r, primes, recips, cap, nbase, g.stream());
+}
+
+int sieve_prepare_base_async(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
+                             uint64_t cap) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!primes || !recips || !nbase) return fail(SIEVE_EINVAL, "NULL buffer");
+  TRY(ensure_ready());
+  CUDA_TRY(sv::launch_prepare(primes, nbase, recips, (uint32_t)cap, g.stream()));
+  g_launches += 1;
+  return 0;
+}
+
+int sieve_stats_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const uint64_t *recips,
+                      const uint32_t *nbase, uint64_t *result) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  TRY(validate(lo, hi));
+  if (!primes || !recips || !nbase || !result) return fail(SIEVE_EINVAL, "NULL buffer");
+  TRY(ensure_ready());
+  return stats_async(make_plan(lo, hi), primes, recips, nbase, result);
+}
+
+int sieve_bitmap_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const uint64_t *recips,
+                       const uint32_t *nbase, uint32_t *out, uint64_t *result) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  TRY(validate(lo, hi));
+  if (!primes || !recips || !nbase || !result) return fail(SIEVE_EINVAL, "NULL buffer");
+  const Plan P = make_plan(lo, hi);
+  if (P.words && !out) return fail(SIEVE_EINVAL, "NULL out");
+  TRY(ensure_ready());
+  return bitmap_async(P, primes, recips, nbase, out, nullptr, result);
+}
+
+int sieve_set_device(int ordinal) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+    return fail(SIEVE_ENODEV, "no CUDA device available");
+  if (ordinal < 0 || ordinal >= ndev) return fail(SIEVE_EINVAL, "device %d out of range", ordinal);
+  if (g.ready && ordinal != g.device)
+    return fail(SIEVE_EINVAL, "device already initialised as %d; call sieve_shutdown first", g.device);
+  g.device = ordinal;
+  CUDA_TRY(cudaSetDevice(ordinal));
+  return 0;
+}
+
+int sieve_set_stream(void *cuda_stream) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  g.user = (cudaStream_t)cuda_stream;
+  g.user_set = cuda_stream != nullptr;
+  return 0;
+}
+
+void *sieve_get_stream(void) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (ensure_ready() < 0) return nullptr;
+  return (void *)g.stream();
+}
+
+int sieve_set_options(const sieve_options *o) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  sieve_options n;
+  default_options(n);
+  if (o) {
+    for (int i = 0; i < 4; ++i)
+      if (o->reserved[i]) return fail(SIEVE_EINVAL, "reserved option fields must be zero");
+    if (o->segment_kb) {
+      if (o->segment_kb != 32 && o->segment_kb != 64 && o->segment_kb != 128 && o->segment_kb != 192)
+        return fail(SIEVE_EINVAL, "segment_kb %u not in {32,64,128,192}", o->segment_kb);
+      n.segment_kb = o->segment_kb;
+    }
+    if (o->wheel) {
+      if (ng_for_wheel(o->wheel) < 0)
+        return fail(SIEVE_EINVAL, "wheel %u not in {19,29,37,43,53,61}", o->wheel);
+      n.wheel = o->wheel;
+    }
+    if (o->threads) {
+      if (o->threads != 256 && o->threads != 512 && o->threads != 1024)
+        return fail(SIEVE_EINVAL, "threads %u not in {256,512,1024}", o->threads);
+      n.threads = o->threads;
+    }
+    if (o->ctas_per_sm > 32) return fail(SIEVE_EINVAL, "ctas_per_sm %u > 32", o->ctas_per_sm);
+    n.ctas_per_sm = o->ctas_per_sm;
+  }
+  g.opt = n;
+  return 0;
+}
+
+int sieve_get_options(sieve_options *o) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!o) return fail(SIEVE_EINVAL, "NULL");
+  if (g.opt.segment_kb == 0) default_options(g.opt);
+  *o = g.opt;
+  return 0;
+}
+
+const char *sieve_last_error(void) { return g_err.c_str(); }
+
+void sieve_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!g.ready) return;
+  cudaStreamSynchronize(g.stream());
+  g.tables.release(); g.primes.release(); g.recips.release(); g.nbase.release();
+  g.partials.release(); g.done.release(); g.result.release(); g.bitmap.release();
+  g.segcnt.release(); g.segoff.release(); g.list.release(); g.items.release(); g.bres.release();
+  if (g.h_res) cudaFreeHost(g.h_res);
+  g.h_res = nullptr;
+  if (g.own) cudaStreamDestroy(g.own);
+  g.own = nullptr;
+  g.smem_limit_set = 0;
+  g.ready = false;
+}
+
+uint64_t sieve_kernel_launches(void) { return g_launches.load(); }
+
+}  // extern "C"

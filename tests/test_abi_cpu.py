@@ -1,0 +1,62 @@
+"""CPU-only checks of the C-ABI library: it builds, loads, exports every
+symbol include/sieve.h declares, validates arguments before touching the
+device, and fails loudly (no CPU fallback) without a GPU."""
+import re
+
+import pytest
+
+import paper_1205_4883_b200 as sv
+from paper_1205_4883_b200 import _abi
+
+HEADER = __import__("os").path.join(__import__("os").path.dirname(__file__), "..", "include", "sieve.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:[a-z_0-9]+\s+\**)+\**(sieve_[a-z_0-9]+)\s*\(", src, re.M)))
+
+
+def test_header_symbols_exported():
+    names = declared_symbols()
+    assert "sieve_count" in names and "sieve_bitmap" in names and "sieve_primes" in names
+    L = sv.lib()
+    for n in names:
+        assert hasattr(L, n), n
+
+
+def test_pure_host_helpers():
+    assert sv.bitmap_words(2, 10**7 + 1) == 156250
+    assert sv.bitmap_words(2, 10**9 + 1) == 15625000
+    assert sv.bitmap_words(5, 5) == 0
+    assert sv.bitmap_words(2, 3) == 0
+    assert sv.bitmap_words(0, 1) == 0
+    assert sv.bitmap_words(0, 2) == 1
+    assert sv.base_capacity(10**5) >= 9591
+    assert sv.base_capacity(1004987) >= 78865
+    assert sv.base_capacity(3161577) >= 227611
+
+
+def test_validation_before_device():
+    with pytest.raises(sv.SieveError) as e:
+        sv.count(10, 5)
+    assert e.value.code == -1
+    with pytest.raises(sv.SieveError) as e:
+        sv.count(0, (1 << 48) + 1)
+    assert e.value.code == -2
+    with pytest.raises(sv.SieveError):
+        sv.set_options(segment_kb=48)
+    with pytest.raises(sv.SieveError):
+        sv.set_options(wheel=23)
+    sv.set_options(segment_kb=64, wheel=61)
+    assert sv.get_options()["segment_kb"] == 64
+    sv.set_options()
+    assert sv.get_options() == {"segment_kb": 192, "wheel": 37, "ctas_per_sm": 0, "threads": 1024}
+
+
+def test_no_cpu_fallback_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(sv.SieveError) as e:
+        sv.count(2, 100)
+    assert e.value.code == -5

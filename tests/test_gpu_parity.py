@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle and pins.
+
+Every comparison is bit-exact (integer work: counts, sums mod 2^64, bitmap
+words, prime lists).  Inputs are seeded (inputs/), sized so the oracle
+finishes in seconds while spanning several segments and a ragged tail; the
+full BASELINE configs are checked against pinned values (tests/golden/) and
+on oracle-computable samples.
+"""
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+import paper_1205_4883_b200 as sv
+from golden_io import kv, subwindows
+from independent import is_prime_td
+
+pytestmark = pytest.mark.gpu
+PINS = kv("config_pins.txt")
+MASK64 = (1 << 64) - 1
+
+
+@pytest.fixture(autouse=True)
+def _defaults():
+    sv.set_options()
+    yield
+    sv.set_options()
+
+
+def _fnv(a):
+    return oracle.fnv1a64(np.ascontiguousarray(a))
+
+
+# ---------------------------------------------------------------- config 1
+def test_config1_count_sum_bitmap_list():
+    lo, hi = inputs.CONFIG1
+    assert sv.count(lo, hi) == int(PINS["config1.count"])
+    assert sv.stats(lo, hi) == (int(PINS["config1.count"]), int(PINS["config1.sum"]))
+    bm, c = sv.bitmap(lo, hi)
+    assert c == int(PINS["config1.count"])
+    assert bm.size == int(PINS["config1.words"])
+    assert _fnv(bm) == int(PINS["config1.fnv"], 16)
+    obm, oc, os_ = oracle.bitmap(lo, hi)
+    assert np.array_equal(bm, obm)
+    lst, c2 = sv.primes(lo, hi)
+    assert c2 == oc
+    assert np.array_equal(lst, oracle.primes(lo, hi))
+    assert int(lst.sum(dtype=np.uint64)) == os_
+
+
+# ------------------------------------------------------- tiny / edge cases
+def test_all_tiny_intervals_exhaustive():
+    isp = [is_prime_td(n) for n in range(257)]
+    los, his = [], []
+    for lo in range(257):
+        for hi in range(lo, 257):
+            los.append(lo)
+            his.append(hi)
+    c, s = sv.batch(los, his)
+    for k, (lo, hi) in enumerate(zip(los, his)):
+        ps = [n for n in range(lo, hi) if isp[n]]
+        assert (int(c[k]), int(s[k])) == (len(ps), sum(ps)), (lo, hi)
+
+
+def test_tiny_intervals_single_calls_and_bitmaps():
+    for lo in range(0, 70):
+        for hi in (lo, lo + 1, lo + 2, lo + 63, lo + 64, lo + 65, lo + 200):
+            assert sv.stats(lo, hi) == oracle.stats(lo, hi, 1), (lo, hi)
+            bm, c = sv.bitmap(lo, hi)
+            obm, oc, _ = oracle.bitmap(lo, hi, 1)
+            assert c == oc
+            assert np.array_equal(bm[:obm.size], obm), (lo, hi)
+            lst, c3 = sv.primes(lo, hi)
+            assert c3 == oc and lst[:c3].tolist() == oracle.primes(lo, hi, threads=1).tolist()
+
+
+def test_errors():
+    with pytest.raises(sv.SieveError):
+        sv.count(10, 5)
+    with pytest.raises(sv.SieveError):
+        sv.count(0, (1 << 48) + 1)
+    assert sv.count(7, 7) == 0
+
+
+def test_p_squared_and_wheel_boundaries():
+    ps = [p for p in range(3, 1200) if is_prime_td(p)]
+    los = [max(0, p * p - 3) for p in ps] + list(range(0, 140))
+    his = [p * p + 4 for p in ps] + [x + 3 for x in range(0, 140)]
+    c, s = sv.batch(los, his)
+    oc, os_ = oracle.batch(los, his, threads=None)
+    assert np.array_equal(c, oc) and np.array_equal(s, os_)
+
+
+# ------------------------------------------------ random seeded intervals
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_intervals_stats(seed):
+    iv = inputs.random_intervals(40, seed=seed, lo_max=10**13, width_max=10**6)
+    for lo, hi in iv[:10]:
+        assert sv.stats(lo, hi) == oracle.stats(lo, hi), (lo, hi)
+    lo = np.array([a for a, _ in iv], dtype=np.uint64)
+    hi = np.array([b for _, b in iv], dtype=np.uint64)
+    c, s = sv.batch(lo, hi)
+    oc, os_ = oracle.batch(lo, hi)
+    assert np.array_equal(c, oc) and np.array_equal(s, os_)
+
+
+@pytest.mark.parametrize("seg_kb", [32, 64, 128, 192])
+@pytest.mark.parametrize("wheel", [19, 37, 61])
+def test_bitmap_multi_segment_ragged(seg_kb, wheel):
+    sv.set_options(segment_kb=seg_kb, wheel=wheel)
+    for lo, hi in [(0, 3 * 10**7 + 17), (10**12 + 3, 10**12 + 2 * 10**7 + 1), (999_999_999_989, 1_000_040_000_000)]:
+        bm, c = sv.bitmap(lo, hi)
+        obm, oc, os_ = oracle.bitmap(lo, hi)
+        assert c == oc
+        assert np.array_equal(bm, obm), (lo, hi, seg_kb, wheel)
+        assert sv.stats(lo, hi) == (oc, os_)
+
+
+@pytest.mark.parametrize("threads", [256, 512, 1024])
+def test_thread_and_occupancy_invariance(threads):
+    sv.set_options(threads=threads, segment_kb=64, ctas_per_sm=2)
+    lo, hi = 10**11, 10**11 + 5 * 10**7 + 3
+    assert sv.stats(lo, hi) == oracle.stats(lo, hi)
+
+
+def test_primes_list_truncation_and_device_out():
+    torch = pytest.importorskip("torch")
+    lo, hi = 10**9, 10**9 + 10**7
+    full = oracle.primes(lo, hi)
+    lst, c = sv.primes(lo, hi, cap=1000)
+    assert c == full.size and lst.tolist() == full[:1000].tolist()
+    _, c0 = sv.primes(lo, hi, cap=0)
+    assert c0 == full.size
+    d = torch.zeros(full.size, dtype=torch.int64, device="cuda")
+    _, c1 = sv.primes(lo, hi, out=d)
+    assert c1 == full.size
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), full)
+    w = sv.bitmap_words(lo, hi)
+    db = torch.zeros(w, dtype=torch.int32, device="cuda")
+    _, cb = sv.bitmap(lo, hi, out=db)
+    obm, oc, _ = oracle.bitmap(lo, hi)
+    assert cb == oc and np.array_equal(db.cpu().numpy().view(np.uint32), obm)
+
+
+def test_repeat_determinism():
+    lo, hi = 2, 2 * 10**8 + 1
+    a = [sv.stats(lo, hi) for _ in range(3)]
+    assert a[0] == a[1] == a[2] == oracle.stats(lo, hi)
+
+
+# ---------------------------------------------------------------- config 2
+@pytest.mark.parametrize("seg_kb", [32, 64, 128, 192])
+def test_config2_bitmap_hash_every_segment_size(seg_kb):
+    sv.set_options(segment_kb=seg_kb)
+    lo, hi = inputs.CONFIG2
+    bm, c = sv.bitmap(lo, hi)
+    assert c == int(PINS["config2.count"])
+    assert bm.size == int(PINS["config2.words"])
+    assert _fnv(bm) == int(PINS["config2.fnv"], 16)
+
+
+def test_config2_vs_oracle_bitmap():
+    lo, hi = inputs.CONFIG2
+    bm, c = sv.bitmap(lo, hi)
+    obm, oc, os_ = oracle.bitmap(lo, hi)
+    assert c == oc and np.array_equal(bm, obm)
+    assert sv.stats(lo, hi) == (oc, os_) == (int(PINS["config2.count"]), int(PINS["config2.sum"]))
+
+
+# ---------------------------------------------------------------- config 3
+def test_config3_count_sum_and_blocks():
+    lo, hi = inputs.CONFIG3
+    assert sv.stats(lo, hi) == (int(PINS["config3.count"]), int(PINS["config3.sum"]))
+    # the G-block split (reading R10): blocks add up, whatever G
+    for G in (2, 4, 8):
+        tot_c, tot_s = 0, 0
+        for g in range(G):
+            a, b = inputs.block_split(lo, hi, g, G)
+            c, s = sv.stats(a, b)
+            tot_c += c
+            tot_s = (tot_s + s) & MASK64
+        assert (tot_c, tot_s) == (int(PINS["config3.count"]), int(PINS["config3.sum"]))
+    # G=2 block values pinned in SURVEY.md 8(c) C3
+    assert sv.stats(2, 5000000003) == (234954223, 572840944428163514)
+    assert sv.stats(5000000003, 10000000001) == (220098288, 1647981488153565724)
+
+
+# ---------------------------------------------------------------- config 4
+def test_config4_count_sum_and_subwindows():
+    lo, hi = inputs.CONFIG4
+    for seg_kb in (32, 192):
+        sv.set_options(segment_kb=seg_kb)
+        assert sv.stats(lo, hi) == (int(PINS["config4.count"]), int(PINS["config4.sum"]))
+    sv.set_options()
+    for (s, c, sm, h) in subwindows():
+        lst, cnt = sv.primes(s, s + 10**7)
+        assert cnt == c
+        assert int(lst.sum(dtype=np.uint64)) == sm
+        assert oracle.fnv1a64(lst.astype("<u8")) == h
+    s0 = subwindows()[0][0]
+    lst, _ = sv.primes(s0, s0 + 10**7)
+    assert np.array_equal(lst, oracle.primes(s0, s0 + 10**7))
+
+
+# ---------------------------------------------------------------- config 5
+def test_config5_batch_digest_and_samples():
+    lo, hi = inputs.config5_intervals()
+    c, s = sv.batch(lo, hi)
+    inter = np.empty(2 * c.size, dtype="<u8")
+    inter[0::2] = c
+    inter[1::2] = s
+    assert int(c.sum()) == int(PINS["config5.count_total"])
+    assert int(s.sum(dtype=np.uint64)) == int(PINS["config5.sum_total"])
+    assert oracle.fnv1a64(inter) == int(PINS["config5.digest"], 16)
+    idx = np.array([0, 1, 2, 3, 4095] + list(range(7, 4096, 409)))
+    oc, os_ = oracle.batch(lo[idx], hi[idx])
+    assert np.array_equal(c[idx], oc) and np.array_equal(s[idx], os_)
