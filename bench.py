@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Headline benchmark: sieved integers/s for pi(N), N = 1e10 (BASELINE.json
+configs[2], "config 3"), count + prime sum, on 1/2/4/8 B200 (one process per
+GPU under torchrun, NCCL over NVLink for the broadcast and the all-reduce).
+
+One step = one pass of the whole hot path:
+  A2 base primes (K1, rank 0) -> A9 NCCL broadcast (N>1) -> A3-A6 segmented
+  sieve of the rank's block (count + sum) -> A9 NCCL all-reduce (N>1).
+
+Timing: W untimed warm-up steps; then K steps bracketed by barrier +
+synchronize on both sides; every step is timed with CUDA events on the
+library stream (the stream the kernels launch on) and L2 is flushed between
+steps outside the events; max over ranks.  `value` = integers of the whole
+range / device seconds per step.  `e2e` = the same metric through the public
+host API (sieve_stats with host outputs, or dist.stats for N>1), host clock.
+
+`--impl reference` times the CPU oracle (the reference arm of this tier) on
+a bounded sample of the same workload on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sieved integers/sec (π(N), N=1e10) at 1/2/4/8 B200; % of roofline"
+UNIT = "integers/s"
+CONFIG3 = (2, 10**10 + 1)
+PI_1E10 = 455052511                  # BASELINE.json north_star
+SUM_1E10 = 2220822432581729238       # SURVEY.md 8(c) C3 (Lucy-Hedgehog)
+WHEEL_ALG = 19                       # M_alg is defined with wheel bound 19
+SMEM_LANES_PER_CLK = 32              # one conflict-free shared-memory wavefront / clk / SM
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--seg-kb", type=int, default=0)
+    ap.add_argument("--wheel", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--no-broadcast", action="store_true",
+                    help="every rank recomputes the base primes instead of the NCCL broadcast")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=4 * 10**9,
+                    help="integers of config 3 the oracle sieves for cpu_baseline")
+    ap.add_argument("--ref-sample", type=int, default=4 * 10**8,
+                    help="integers per --impl reference step")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """pynvml sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- roofline
+def algorithmic_marks(lo: int, hi: int, wheel: int = WHEEL_ALG) -> int:
+    """M_alg: number of (odd prime p, odd multiple m) pairs with wheel < p <=
+    isqrt(hi-1) and max(lo, p^2) <= m < hi -- the marks the method must make
+    beyond the wheel."""
+    import numpy as np
+    if hi <= lo or hi < 10:
+        return 0
+    r = math.isqrt(hi - 1)
+    s = np.ones(r + 1, dtype=bool)
+    s[:2] = False
+    for q in range(2, math.isqrt(r) + 1):
+        if s[q]:
+            s[q * q::q] = False
+    p = np.nonzero(s)[0].astype(object)
+    p = [int(x) for x in p if x > wheel]
+    total = 0
+    for q in p:
+        a = max(lo, q * q)
+        m0 = ((a + q - 1) // q) * q
+        if m0 % 2 == 0:
+            m0 += q
+        if m0 < hi:
+            total += (hi - 1 - m0) // (2 * q) + 1
+    return total
+
+
+def load_traffic():
+    """dram bytes per launch of the sieve kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_sieve_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import oracle
+    lo = CONFIG3[0]
+    n = min(args.ref_sample, CONFIG3[1] - lo)
+    cores = oracle.default_threads()
+    for _ in range(args.warmup):
+        oracle.stats(lo, lo + min(n, 10**7), cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.stats(lo, lo + n, cores)
+        times.append(time.perf_counter() - t0)
+    per = sum(times) / len(times)
+    value = n / per
+    sample = f"[2, {lo + n}) of config 3 ({n} integers) per step, count+sum, {cores} threads"
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic", "config": {"workload": "config3: pi(1e10) count+sum (oracle sample)",
+                                        "sample_integers": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def cpu_baseline(args):
+    import oracle
+    cores = oracle.default_threads()
+    lo = CONFIG3[0]
+    n = min(args.cpu_sample, CONFIG3[1] - lo)
+    t0 = time.perf_counter()
+    oracle.stats(lo, lo + n, cores)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"[2, {lo + n}) = first {n} integers of config 3, count+sum, one run, "
+                      f"{dt:.2f} s"}
+
+
+# ----------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as tdist
+
+    import paper_1205_4883_b200 as sv
+    from paper_1205_4883_b200 import dist as D
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+    sv.set_device(local)
+    stream = torch.cuda.Stream(device=dev)
+    sv.set_stream(stream)
+    sv.set_options(segment_kb=args.seg_kb, wheel=args.wheel, threads=args.threads,
+                   ctas_per_sm=args.ctas_per_sm)
+    opts = sv.get_options()
+
+    lo, hi = CONFIG3
+    r = math.isqrt(hi - 1)
+    base = D.alloc_base(sv.base_capacity(r), dev)
+    result = torch.zeros(2, dtype=torch.int64, device=dev)
+    a, b = D.block_of(lo, hi, rank, world)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    bcast = world > 1 and not args.no_broadcast
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+
+    def step(e=None):
+        with torch.cuda.stream(stream):
+            if e: e[0].record(stream)
+            if rank == 0 or not bcast:
+                sv.base_primes_async(r, base.primes, base.recips, base.nbase)
+            if bcast:
+                tdist.broadcast(base.packed, src=0)
+            if e: e[1].record(stream)
+            sv.stats_async(a, b, base.primes, base.recips, base.nbase, result)
+            if e: e[2].record(stream)
+            if world > 1:
+                tdist.all_reduce(result, op=tdist.ReduceOp.SUM)
+            if e: e[3].record(stream)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    got = [D.i64_to_u64(x) for x in result.cpu().tolist()]
+    verified = (got[0] == PI_1E10 and got[1] == SUM_1E10)
+
+    launches0 = sv.kernel_launches()
+    sampler = ClockSampler(local)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.perf_counter()
+    with sampler:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # L2 flush, outside the events
+            step(ev[k])
+        torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall0
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    launches = sv.kernel_launches() - launches0
+
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    sieve_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    base_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    tot = torch.tensor([sum(step_ms), sum(sieve_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(tot, op=tdist.ReduceOp.MAX)
+    ms_per_step = tot[0].item() / args.steps
+    sieve_ms_mean = tot[1].item() / args.steps
+    value = (hi - lo) / (ms_per_step / 1e3)
+
+    # e2e: the public API with host outputs, host clock, K steps
+    if world == 1:
+        for _ in range(2):
+            sv.stats(lo, hi)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            c, s = sv.stats(lo, hi)
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        verified = verified and (c, s) == (PI_1E10, SUM_1E10)
+    else:
+        for _ in range(2):
+            D.stats(lo, hi)
+        tdist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            c, s = D.stats(lo, hi)
+        tdist.barrier()
+        e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        tdist.all_reduce(e2e_t, op=tdist.ReduceOp.MAX)
+        e2e_s = e2e_t.item() / args.steps
+        verified = verified and (c, s) == (PI_1E10, SUM_1E10)
+
+    if rank == 0:
+        clocks = sampler.summary()
+        peaks = load_peaks()
+        sm_max = peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0
+        m_alg = algorithmic_marks(a, b)  # rank 0's block (the whole range at N=1)
+        achieved = m_alg / (sieve_ms_mean / 1e3) / 1e9
+        peak = 148 * SMEM_LANES_PER_CLK * sm_max * 1e6 / 1e9
+        roof = {"bound": "smem_atomic", "achieved": achieved, "peak": peak, "unit": "Gmarks/s",
+                "frac": achieved / peak, "traffic": load_traffic(),
+                "kernel": "sv::k_sieve<NG,kCount>", "marks_alg_per_launch": m_alg,
+                "peak_basis": f"148 SMs x {SMEM_LANES_PER_CLK} shared-memory lanes/clk x "
+                              f"{sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
+                "kernel_ms": sieve_ms_mean, "kernel_share_of_step": sieve_ms_mean / ms_per_step}
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "config3: pi(1e10) count + prime sum over [2, 1e10+1)",
+                       "lo": lo, "hi": hi, "segment_kb": opts["segment_kb"], "wheel": opts["wheel"],
+                       "threads": opts["threads"], "base_primes": "broadcast" if bcast else "per-rank",
+                       "l2": "flushed (256 MiB write) between timed steps, outside the events",
+                       "parallelism": f"range split over {world} GPU(s)"},
+            "verified": verified,
+            "base_ms": statistics.mean(base_ms),
+            "wall_ms_per_step_incl_flush": t_wall * 1e3 / args.steps,
+            "roofline": roof,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "e2e": {"value": (hi - lo) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16,
+                    "d2h_bytes_per_step": 16, "ms_per_step": e2e_s * 1e3,
+                    "api": "sieve_stats (host outputs)" if world == 1 else "dist.stats"},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -77,22 +77,3 @@ def random_intervals(n: int, seed: int, lo_max: int, width_max: int) -> list[tup
         w = g.next() % (width_max + 1)
         out.append((a, a + w))
     return out
-
-
-def block_split(lo: int, hi: int, g: int, G: int) -> tuple[int, int]:
-    """Reading R10 (plumbing, no sieve arithmetic): block g of G equal
-    contiguous blocks of [lo, hi) on the odd-only word grid, i.e. block
-    boundaries at o0 + 64*floor(g*words/G) with o0 = lo|1, clipped to
-    [lo, hi].  Block 0 starts at lo, the last ends at hi."""
-    if hi <= lo:
-        return lo, hi
-    o0 = lo | 1
-    B = hi // 2 - lo // 2
-    words = (B + 31) // 32
-    def edge(k: int) -> int:
-        if k <= 0:
-            return lo
-        if k >= G:
-            return hi
-        return min(hi, o0 + 64 * ((k * words) // G))
-    return edge(g), edge(g + 1)

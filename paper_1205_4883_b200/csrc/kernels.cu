@@ -86,29 +86,50 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // the 32 lanes of a warp read 32 consecutive table words (conflict-free) and
 // funnel-shift each window into place.  Words up to the end of the last quad
 // are written so that the epilogue can read whole uint4 quads.
+template <int G>
+struct WheelGroup {
+  static constexpr uint32_t P = group_period(G);
+  static constexpr uint32_t OFF = group_offset(G);
+};
+
+// OR the window of groups G..NG-1 for the current word and advance their
+// table indices (compile-time recursion: every modulus is a constant).
+template <int G, int NG>
+__device__ __forceinline__ uint32_t wheel_word(const uint32_t *tab, uint32_t (&ig)[NG],
+                                               const uint32_t (&dg)[NG]) {
+  if constexpr (G == NG) {
+    return 0u;
+  } else {
+    constexpr uint32_t P = WheelGroup<G>::P;
+    const uint32_t *t = tab + WheelGroup<G>::OFF + (ig[G] >> 5);
+    const uint32_t v = __funnelshift_r(t[0], t[1], ig[G] & 31u);
+    ig[G] += dg[G];
+    if (ig[G] >= P) ig[G] -= P;
+    return v | wheel_word<G + 1, NG>(tab, ig, dg);
+  }
+}
+
+template <int G, int NG>
+__device__ __forceinline__ void wheel_setup(uint32_t (&ig)[NG], uint32_t (&dg)[NG], uint64_t base,
+                                            uint32_t tid, uint32_t nt) {
+  if constexpr (G < NG) {
+    constexpr uint32_t P = WheelGroup<G>::P;
+    ig[G] = (uint32_t)((base % P + (32u * tid) % P) % P);
+    dg[G] = (32u * nt) % P;
+    wheel_setup<G + 1, NG>(ig, dg, base, tid, nt);
+  }
+}
+
 template <int NG>
 __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, uint64_t o0,
                                            uint64_t bit0, uint32_t valid, uint64_t a) {
   const uint32_t nt = blockDim.x, tid = threadIdx.x;
   const uint32_t nwords = ((valid + 127u) >> 7) << 2;
   // table index of word w: ((o0-1)/2 + bit0 + 32*w) mod P_g
-  const uint64_t base = ((o0 - 1) >> 1) + bit0;
   uint32_t ig[NG], dg[NG];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    const uint32_t P = group_period(g);
-    ig[g] = (uint32_t)((base % P + (uint64_t)(32u * tid) % P) % P);
-    dg[g] = (32u * nt) % P;
-  }
+  wheel_setup<0, NG>(ig, dg, ((o0 - 1) >> 1) + bit0, tid, nt);
   for (uint32_t w = tid; w < nwords; w += nt) {
-    uint32_t v = 0;
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      const uint32_t *t = tab + group_offset(g) + (ig[g] >> 5);
-      v |= __funnelshift_r(t[0], t[1], ig[g] & 31u);
-      ig[g] += dg[g];
-      if (ig[g] >= group_period(g)) ig[g] -= group_period(g);
-    }
+    uint32_t v = wheel_word<0, NG>(tab, ig, dg);
     const uint64_t n0 = a + 64ull * w;  // odd integer of the word's bit 0
     if (n0 <= wheel_bound(NG)) {
       for (uint32_t b = 0; b < 32u && n0 + 2ull * b <= wheel_bound(NG); ++b) {

@@ -1,0 +1,194 @@
+"""Multi-GPU orchestration (step A9 and the multi-GPU half of A10).
+
+One process per GPU (torchrun), torch.distributed process groups over NCCL
+for the plumbing -- the paper's Fig. 6 flow (partition ->
+distribute -> sieve -> gather, read as SPEC.md:10/271/296) re-expressed for
+one NVSwitch box:
+
+  partition : equal contiguous blocks of the odd-only word grid
+              (reading R10; "average divide data into nodes")
+  distribute: rank 0 computes the base primes (K1) and broadcasts ONE packed
+              buffer [recips | primes | nbase] (PAPER.md:19's FIFO buffer of
+              data from other nodes becomes a single NCCL broadcast)
+  sieve     : every rank runs the segmented sieve on its block (CUDA, C ABI)
+  gather    : one all-reduce of u64[2] = {count, sum}; two's-complement int64
+              addition is bit-identical to u64 addition mod 2^64.
+
+The compute callables default to the CUDA library; tests may inject others
+to exercise this host logic with the gloo backend on CPU.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+MASK64 = (1 << 64) - 1
+
+
+def isqrt(x: int) -> int:
+    return math.isqrt(x) if x > 0 else 0
+
+
+def block_of(lo: int, hi: int, rank: int, world: int) -> tuple[int, int]:
+    """Step A1 across GPUs (reading R10): block `rank` of `world` equal
+    contiguous blocks of [lo, hi) on the odd-only word grid.  Boundaries sit
+    at o0 + 64*floor(k*words/world) (o0 = lo|1), clipped to [lo, hi], so
+    every block's bitmap starts on a 32-bit word of the whole range's bitmap
+    and the blocks tile [lo, hi) exactly."""
+    if hi <= lo:
+        return lo, hi
+    o0 = lo | 1
+    words = (hi // 2 - lo // 2 + 31) // 32
+
+    def edge(k: int) -> int:
+        if k <= 0:
+            return lo
+        if k >= world:
+            return hi
+        return min(hi, o0 + 64 * ((k * words) // world))
+
+    return edge(rank), edge(rank + 1)
+
+
+class CudaBackend:
+    """The product compute path: the C-ABI library on the current device."""
+
+    def base_capacity(self, r):
+        import paper_1205_4883_b200 as sv
+        return sv.base_capacity(r)
+
+    def base_primes(self, r, base):
+        import paper_1205_4883_b200 as sv
+        sv.base_primes_async(r, base.primes, base.recips, base.nbase)
+
+    def stats(self, a, b, base, result):
+        import paper_1205_4883_b200 as sv
+        sv.stats_async(a, b, base.primes, base.recips, base.nbase, result)
+
+
+def u64_to_i64(x: int) -> int:
+    x &= MASK64
+    return x - (1 << 64) if x >= (1 << 63) else x
+
+
+def i64_to_u64(x: int) -> int:
+    return x & MASK64
+
+
+@dataclass
+class BaseBuffers:
+    """Views into one packed device buffer: recips (u64) | primes (u32) | nbase."""
+    packed: "object"
+    recips: "object"
+    primes: "object"
+    nbase: "object"
+    cap: int
+
+
+def alloc_base(cap: int, device) -> BaseBuffers:
+    import torch
+    n32 = 2 * cap + cap + 1
+    packed = torch.zeros(n32, dtype=torch.int32, device=device)
+    recips = packed[: 2 * cap].view(torch.int64)
+    primes = packed[2 * cap: 3 * cap]
+    nbase = packed[3 * cap: 3 * cap + 1]
+    return BaseBuffers(packed, recips, primes, nbase, cap)
+
+
+def stats(lo: int, hi: int, group=None, broadcast: bool = True, base: BaseBuffers | None = None,
+          result=None, sync: bool = True, backend=None, device=None):
+    """pi-count and prime sum of [lo, hi) over all ranks of `group` (public
+    multi-GPU API).  Returns (count, sum mod 2^64) on every rank when sync,
+    else the device result tensor (int64[2], already all-reduced)."""
+    import torch
+    import torch.distributed as dist
+
+    be = backend if backend is not None else CudaBackend()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    r = isqrt(hi - 1) if hi >= 2 else 0
+    if base is None:
+        base = alloc_base(be.base_capacity(r), dev)
+    if result is None:
+        result = torch.zeros(2, dtype=torch.int64, device=dev)
+    if rank == 0 or not broadcast or world == 1:
+        be.base_primes(r, base)
+    if world > 1 and broadcast:
+        dist.broadcast(base.packed, src=0, group=group)
+    a, b = block_of(lo, hi, rank, world)
+    be.stats(a, b, base, result)
+    if world > 1:
+        dist.all_reduce(result, op=dist.ReduceOp.SUM, group=group)
+    if not sync:
+        return result
+    h = result.cpu().tolist()
+    return i64_to_u64(h[0]), i64_to_u64(h[1])
+
+
+# ---------------------------------------------------------------- batch / LPT
+def batch_cost(lo: np.ndarray, hi: np.ndarray, seg_bits: int = 192 * 8192) -> np.ndarray:
+    """Cost model of one interval (A10): odd slots to sieve plus one
+    first-hit reduction per (segment, base prime).  pi(sqrt(hi)) is
+    approximated by sqrt(hi)/ln(sqrt(hi)) -- only the ranking matters."""
+    lo = lo.astype(np.float64)
+    hi = hi.astype(np.float64)
+    width = np.maximum(hi - lo, 0.0)
+    rt = np.sqrt(np.maximum(hi, 4.0))
+    nprimes = rt / np.log(rt)
+    nseg = np.ceil(width / 2.0 / seg_bits)
+    return 0.6 * width / 2.0 + 20.0 * nseg * nprimes
+
+
+def lpt_assign(cost: np.ndarray, world: int) -> list[np.ndarray]:
+    """Longest-processing-time-first: intervals in decreasing cost, each to
+    the currently least-loaded rank.  Deterministic (stable sort, ties to the
+    lowest rank)."""
+    order = np.argsort(-cost, kind="stable")
+    load = np.zeros(world)
+    parts: list[list[int]] = [[] for _ in range(world)]
+    for i in order:
+        k = int(np.argmin(load))
+        parts[k].append(int(i))
+        load[k] += cost[i]
+    return [np.array(sorted(p), dtype=np.int64) for p in parts]
+
+
+def batch(lo, hi, group=None, batch_fn=None, device=None):
+    """Per-interval (count, sum) over all ranks: LPT assignment, local batch
+    on each rank, all_gather of the padded per-rank results, reassembly in
+    input order.  Every rank returns the full arrays."""
+    import torch
+    import torch.distributed as dist
+
+    lo = np.ascontiguousarray(lo, dtype=np.uint64)
+    hi = np.ascontiguousarray(hi, dtype=np.uint64)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if batch_fn is None:
+        import paper_1205_4883_b200 as sv
+        batch_fn = sv.batch
+    parts = lpt_assign(batch_cost(lo, hi), world)
+    mine = parts[rank]
+    c, s = batch_fn(lo[mine], hi[mine])
+    if world == 1:
+        return np.asarray(c, dtype=np.uint64), np.asarray(s, dtype=np.uint64)
+    width = max(len(p) for p in parts)
+    dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
+                                             if torch.cuda.is_available() else torch.device("cpu"))
+    loc = np.zeros((width, 2), dtype=np.uint64)
+    loc[: len(mine), 0] = c
+    loc[: len(mine), 1] = s
+    t = torch.from_numpy(loc.view(np.int64)).to(dev)
+    outs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(outs, t, group=group)
+    count = np.zeros(lo.size, dtype=np.uint64)
+    ssum = np.zeros(lo.size, dtype=np.uint64)
+    for k in range(world):
+        arr = outs[k].cpu().numpy().view(np.uint64)
+        idx = parts[k]
+        count[idx] = arr[: len(idx), 0]
+        ssum[idx] = arr[: len(idx), 1]
+    return count, ssum

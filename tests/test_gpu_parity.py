@@ -12,6 +12,7 @@ import pytest
 import inputs
 import oracle
 import paper_1205_4883_b200 as sv
+from paper_1205_4883_b200.dist import block_of
 from golden_io import kv, subwindows
 from independent import is_prime_td
 
@@ -175,7 +176,7 @@ def test_config3_count_sum_and_blocks():
     for G in (2, 4, 8):
         tot_c, tot_s = 0, 0
         for g in range(G):
-            a, b = inputs.block_split(lo, hi, g, G)
+            a, b = block_of(lo, hi, g, G)
             c, s = sv.stats(a, b)
             tot_c += c
             tot_s = (tot_s + s) & MASK64
