@@ -103,8 +103,8 @@ __device__ __forceinline__ uint32_t wheel_word(const uint32_t *tab, uint32_t (&i
     constexpr uint32_t P = WheelGroup<G>::P;
     const uint32_t *t = tab + WheelGroup<G>::OFF + (ig[G] >> 5);
     const uint32_t v = __funnelshift_r(t[0], t[1], ig[G] & 31u);
-    ig[G] += dg[G];
-    if (ig[G] >= P) ig[G] -= P;
+    const uint32_t x = ig[G] + dg[G];
+    ig[G] = min(x, x - P);  // x < 2P: x - P wraps above x when x < P
     return v | wheel_word<G + 1, NG>(tab, ig, dg);
   }
 }
@@ -128,7 +128,15 @@ __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, u
   // table index of word w: ((o0-1)/2 + bit0 + 32*w) mod P_g
   uint32_t ig[NG], dg[NG];
   wheel_setup<0, NG>(ig, dg, ((o0 - 1) >> 1) + bit0, tid, nt);
-  for (uint32_t w = tid; w < nwords; w += nt) {
+  // fast path: words with no fix-up (first integer > w) and no tail slot
+  const uint64_t nfix = a > wheel_bound(NG) ? 0ull : (wheel_bound(NG) - a) / 64 + 1;
+  const uint32_t wfast_lo = nfix < nwords ? (uint32_t)nfix : nwords;
+  const uint32_t wfast_hi = valid >> 5;  // words [.., valid/32) are entirely valid
+  uint32_t w = tid;
+  if (wfast_lo == 0) {
+    for (; w < wfast_hi; w += nt) seg[w] = wheel_word<0, NG>(tab, ig, dg);
+  }
+  for (; w < nwords; w += nt) {
     uint32_t v = wheel_word<0, NG>(tab, ig, dg);
     const uint64_t n0 = a + 64ull * w;  // odd integer of the word's bit 0
     if (n0 <= wheel_bound(NG)) {
@@ -151,16 +159,37 @@ struct PrimeRegions {
   uint32_t end;    // first prime > r
 };
 
+// Mark bit `mask` of the words at byte offsets A, A+step, ... < alim of the
+// segment: the hits of one lane that share a bit position (2-3 instructions
+// per mark: the address add and the atomic, plus a guard per 4 marks).
+__device__ __forceinline__ void mark_run(char *segb, uint32_t A, uint32_t alim, uint32_t step,
+                                         uint32_t mask) {
+  for (; A + 3u * step < alim; A += 4u * step) {
+    atomicOr(reinterpret_cast<uint32_t *>(segb + A), mask);
+    atomicOr(reinterpret_cast<uint32_t *>(segb + A + step), mask);
+    atomicOr(reinterpret_cast<uint32_t *>(segb + A + 2u * step), mask);
+    atomicOr(reinterpret_cast<uint32_t *>(segb + A + 3u * step), mask);
+  }
+  if (A < alim) {
+    atomicOr(reinterpret_cast<uint32_t *>(segb + A), mask);
+    if (A + step < alim) {
+      atomicOr(reinterpret_cast<uint32_t *>(segb + A + step), mask);
+      if (A + 2u * step < alim) atomicOr(reinterpret_cast<uint32_t *>(segb + A + 2u * step), mask);
+    }
+  }
+}
+
 // A4/A5: mark the odd multiples of every base prime in [R.start, R.end).
 //
-// Three regions by hits per segment K ~ S/p:
-//  (i)  small primes (K >= kSmallHits): the hits k = r + 32m of residue class
-//       r (mod 32) all have the same bit (j0 + r p) & 31 and sit exactly p
-//       words apart, so lane l takes m = l + 32s: the 32 lanes of an atomic
-//       hit 32 distinct banks (p odd) with one warp-uniform mask, and a lane
-//       advances its byte address by 128 p per atomic (2 instructions/mark).
-//  (ii) medium primes: one prime per warp, lanes take consecutive hits.
-//  (iii) large primes (K < kLaneHits): one prime per lane.
+// Hit k of prime p in the segment is slot j0 + k p.  Hits k and k + 32 have
+// the same bit (32 p bits = p whole words apart), so a lane that walks every
+// 32nd hit keeps one mask and adds 4p to a byte address per atomic.  Regions
+// by hits per segment K ~ S/p:
+//  (i)  small primes (K >= kSmallHits): residue class r (mod 32) per warp,
+//       lane l takes hits r + 32 l + 1024 s: the 32 lanes of one atomic are
+//       p words apart, i.e. in 32 distinct banks for any odd p.
+//  (ii) medium primes: one prime per warp, lane l takes hits l + 32 s.
+//  (iii) large primes (K < kLaneHits): one prime per lane, unrolled by 4.
 // First hits are computed 32 primes at a time (one Barrett reduction per
 // lane) and broadcast with shuffles.
 __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__restrict__ primes,
@@ -188,18 +217,8 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
         const uint32_t jr = j0 + r * p;  // first hit of residue class r
         if (jr >= valid) break;
         const uint32_t bit = jr & 31u;
-        const uint32_t mask = 1u << bit;
-        const uint32_t alim = (vw + (bit < vb ? 1u : 0u)) << 2;
-        const uint32_t step = 128u * p;
-        uint32_t A = ((jr >> 5) + lane * p) << 2;
-        // byte offsets: 4 atomics per guard, then the remainder
-        for (; A + 3u * step < alim; A += 4u * step) {
-          atomicOr(reinterpret_cast<uint32_t *>(segb + A), mask);
-          atomicOr(reinterpret_cast<uint32_t *>(segb + A + step), mask);
-          atomicOr(reinterpret_cast<uint32_t *>(segb + A + 2u * step), mask);
-          atomicOr(reinterpret_cast<uint32_t *>(segb + A + 3u * step), mask);
-        }
-        for (; A < alim; A += step) atomicOr(reinterpret_cast<uint32_t *>(segb + A), mask);
+        mark_run(segb, ((jr >> 5) + lane * p) << 2, (vw + (bit < vb ? 1u : 0u)) << 2, 128u * p,
+                 1u << bit);
       }
     }
   }
@@ -216,17 +235,26 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
       const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
       const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
       if (j0 == kNone) { stop = true; break; }
-      const uint32_t stride = 32u * p;
-      for (uint32_t j = j0 + lane * p; j < valid; j += stride) mark(seg, j);
+      const uint32_t j = j0 + lane * p;  // this lane's first hit
+      if (j < valid) {
+        const uint32_t bit = j & 31u;
+        mark_run(segb, (j >> 5) << 2, (vw + (bit < vb ? 1u : 0u)) << 2, 4u * p, 1u << bit);
+      }
     }
     if (stop) break;
   }
   // (iii) large primes: lane per prime (few hits each)
   for (uint32_t k = R.lanes + threadIdx.x; k < R.end; k += blockDim.x) {
     const uint32_t p = __ldg(primes + k);
-    const uint32_t j0 = first_hit(a, seg_end, p, __ldg(recips + k));
-    if (j0 == kNone) break;
-    for (uint32_t j = j0; j < valid; j += p) mark(seg, j);
+    uint32_t j = first_hit(a, seg_end, p, __ldg(recips + k));
+    if (j == kNone) break;
+    for (; j + 3u * p < valid; j += 4u * p) {
+      mark(seg, j);
+      mark(seg, j + p);
+      mark(seg, j + 2u * p);
+      mark(seg, j + 3u * p);
+    }
+    for (; j < valid; j += p) mark(seg, j);
   }
 }
 
