@@ -56,8 +56,8 @@ extern "C" {
 
 /* Tuning options (sieve_set_options).  Zero fields mean "default". */
 typedef struct sieve_options {
-    uint32_t segment_kb;  /* shared-memory segment size in KiB: 32, 64, 128 or 192 (default 192) */
-    uint32_t wheel;       /* wheel bound w (pre-sieved primes 3..w): 19, 29, 37, 43, 53 or 61 (default 43) */
+    uint32_t segment_kb;  /* shared-memory segment size in KiB: a multiple of 16 in [16, 208] (default 208) */
+    uint32_t wheel;       /* wheel bound w (pre-sieved primes 3..w): 19, 29, 37, 43, 53 or 61 (default 37) */
     uint32_t ctas_per_sm; /* resident CTAs per SM for the sieve kernel (default: occupancy maximum) */
     uint32_t threads;     /* threads per CTA: 256, 512 or 1024 (default 1024) */
     uint32_t reserved[4]; /* must be zero */
@@ -142,6 +142,13 @@ void sieve_shutdown(void);
 
 /* Number of kernels this library launched since load (evidence counter). */
 uint64_t sieve_kernel_launches(void);
+
+/* Diagnostics: when dev_counters (device, 8 x uint64, zeroed by the caller)
+ * is non-NULL, later sieve launches add SM-clock cycles per phase:
+ * [0] wheel init, [1] marking, [2] count/write-back (CTA level, summed over
+ * segments), [3] small-, [4] medium-, [5] large-prime marking (per warp,
+ * summed over warps), [6] segments.  NULL disables (the default). */
+int sieve_debug_set_profile(uint64_t *dev_counters);
 
 #ifdef __cplusplus
 }

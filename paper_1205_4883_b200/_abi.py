@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-library_path = os.path.join(_HERE, "libsieve.so")
+# SIEVE_LIBRARY overrides the path (tuning experiments with variant builds)
+library_path = os.environ.get("SIEVE_LIBRARY") or os.path.join(_HERE, "libsieve.so")
 
 SIEVE_MAX_HI = 1 << 48
 _ERRNAMES = {-1: "SIEVE_EINVAL", -2: "SIEVE_ERANGE", -3: "SIEVE_ENOMEM", -4: "SIEVE_ECUDA",
@@ -66,6 +67,7 @@ def lib():
             "sieve_last_error": (ctypes.c_char_p, []),
             "sieve_shutdown": (None, []),
             "sieve_kernel_launches": (_u64, []),
+            "sieve_debug_set_profile": (ctypes.c_int, [_p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -198,6 +200,11 @@ def get_options() -> dict:
 
 def shutdown() -> None:
     lib().sieve_shutdown()
+
+
+def debug_set_profile(counters_t) -> None:
+    """Diagnostics: phase-cycle counters (torch int64[8] CUDA tensor) or None."""
+    _check(lib().sieve_debug_set_profile(_ptr(counters_t)))
 
 
 def kernel_launches() -> int:

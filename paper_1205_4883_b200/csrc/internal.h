@@ -46,10 +46,22 @@ constexpr uint64_t kOddPrimesBelow64 =
     (1ull << 43) | (1ull << 47) | (1ull << 53) | (1ull << 59) | (1ull << 61);
 
 // Marking-work partition (step A4): primes with at least kSmallHits hits per
-// segment are marked by residue class mod 32 (conflict-free atomics).
-constexpr uint32_t kSmallHits = 4096;
+// segment are marked by residue class mod 32 across warps (conflict-free
+// atomics); primes with kSkewHits <= K < kSmallHits one per warp, one residue
+// class per lane with rotated starts (conflict-free atomics).
+#ifndef SIEVE_SMALL_HITS
+#define SIEVE_SMALL_HITS 16384
+#endif
+constexpr uint32_t kSmallHits = SIEVE_SMALL_HITS;
+#ifndef SIEVE_SKEW_HITS
+#define SIEVE_SKEW_HITS 1024
+#endif
+constexpr uint32_t kSkewHits = SIEVE_SKEW_HITS;
 // primes with fewer than kLaneHits hits per segment are marked lane-per-prime
-constexpr uint32_t kLaneHits = 64;
+#ifndef SIEVE_LANE_HITS
+#define SIEVE_LANE_HITS 128
+#endif
+constexpr uint32_t kLaneHits = SIEVE_LANE_HITS;
 
 // One work item of the batch kernel (step A10): one segment of one interval.
 struct BatchItem {
@@ -79,6 +91,7 @@ struct SieveParams {
   unsigned int *done;      // last-block-done ticket (self-resetting)
   uint64_t *result;        // [2] count, sum mod 2^64 (batch: [2 * nintervals])
   const BatchItem *items;  // batch mode
+  unsigned long long *prof;  // optional phase-cycle counters (diagnostics), [8]
 };
 
 enum Mode { kCount = 0, kBitmap = 1, kBatch = 2 };

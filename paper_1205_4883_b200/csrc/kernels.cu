@@ -155,6 +155,7 @@ __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, u
 struct PrimeRegions {
   uint32_t start;  // first marking prime (after the wheel primes)
   uint32_t mid;    // first prime with fewer than kSmallHits hits per full segment
+  uint32_t skew;   // first prime with fewer than kSkewHits hits per full segment
   uint32_t lanes;  // first prime with fewer than kLaneHits hits per full segment
   uint32_t end;    // first prime > r
 };
@@ -183,18 +184,24 @@ __device__ __forceinline__ void mark_run(char *segb, uint32_t A, uint32_t alim, 
 //
 // Hit k of prime p in the segment is slot j0 + k p.  Hits k and k + 32 have
 // the same bit (32 p bits = p whole words apart), so a lane that walks every
-// 32nd hit keeps one mask and adds 4p to a byte address per atomic.  Regions
-// by hits per segment K ~ S/p:
-//  (i)  small primes (K >= kSmallHits): residue class r (mod 32) per warp,
-//       lane l takes hits r + 32 l + 1024 s: the 32 lanes of one atomic are
-//       p words apart, i.e. in 32 distinct banks for any odd p.
-//  (ii) medium primes: one prime per warp, lane l takes hits l + 32 s.
-//  (iii) large primes (K < kLaneHits): one prime per lane, unrolled by 4.
-// First hits are computed 32 primes at a time (one Barrett reduction per
-// lane) and broadcast with shuffles.
+// 32nd hit -- one residue class mod 32 -- keeps one mask and adds 4p to a byte
+// address per atomic.  Regions by hits per segment K ~ S/p (DESIGN.md
+// "Marking"):
+//  (i)  K >= kSkewHits: work units of kPieceHits consecutive hits of one
+//       prime, round robin over warps.  Lane l owns residue class l of the
+//       unit; its word at class step m is W_l + p m.  The lane starts its
+//       class at the rotation sigma_l = (l - W_l) p^-1 (mod 32) and walks it
+//       in rounds of 32 steps (mod 32), so at step t its bank is l + p t
+//       (mod 32): the 32 lanes of every atomic hit 32 distinct banks.
+//  (ii) 64 <= K < kSkewHits: one prime per warp, lane l takes hits l + 32 s.
+//  (iii) K < kLaneHits: one prime per lane, unrolled by 4.
+// Region (ii) computes first hits 32 primes at a time (one Barrett reduction
+// per lane) and broadcasts them with shuffles.
 __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__restrict__ primes,
                                              const uint64_t *__restrict__ recips,
-                                             const PrimeRegions R, uint64_t a, uint32_t valid) {
+                                             const PrimeRegions R,
+                                             uint64_t a, uint32_t valid, unsigned long long *prof) {
+  const long long t0 = prof ? clock64() : 0;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t seg_end = a + 2ull * valid;
   char *segb = reinterpret_cast<char *>(seg);
@@ -222,8 +229,50 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
       }
     }
   }
-  // (ii) medium primes: prime i = R.mid + warp + nw*t, batches of 32 t's
-  for (uint32_t ib = R.mid + warp; ib < R.lanes; ib += 32u * nw) {
+  const long long t1 = prof ? clock64() : 0;
+  // (ii-a) medium primes with >= kSkewHits hits: one prime per warp, lane l
+  // owns residue class l (hits l + 32m, one bit, words W_l + p m).  The lane
+  // starts its class at a rotation sigma_l chosen so that its bank at step t
+  // is l + p t (mod 32): all 32 lanes of every atomic in distinct banks.
+  // Rotation is mod 32 hits, which shifts a word by 32 p == 0 (mod 32) banks.
+  for (uint32_t ib = R.mid + warp; ib < R.skew; ib += 32u * nw) {
+    const uint32_t i = ib + lane * nw;
+    uint32_t pl = 0, jl = kNone;
+    if (i < R.skew) {
+      pl = __ldg(primes + i);
+      jl = first_hit(a, seg_end, pl, __ldg(recips + i));
+    }
+    bool stop = false;
+    for (uint32_t k = 0; k < 32u; ++k) {
+      const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
+      const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
+      if (j0 == kNone) { stop = true; break; }
+      const uint32_t j = j0 + lane * p;          // first hit of class `lane`
+      const uint32_t bit = j & 31u, mask = 1u << bit;
+      const uint32_t w = j >> 5;
+      const uint32_t alim = (vw + (bit < vb ? 1u : 0u)) << 2;
+      const uint32_t step = 4u * p, span = 128u * p;
+      const uint32_t pinv = p * (2u - p * p);     // p^-1 mod 32 (Newton step from p^-1 = p mod 8)
+      uint32_t o = (((lane - w) * pinv) & 31u) * step;
+      uint32_t B = w << 2;
+      const uint32_t nh = B < alim ? (alim - B + step - 1u) / step : 0u;  // hits of this class
+      const uint32_t full = nh >> 5;  // lanes differ by at most one chunk
+      for (uint32_t c = 0; c < full; ++c, B += span) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          atomicOr(reinterpret_cast<uint32_t *>(segb + B + o), mask);
+          const uint32_t x = o + step;
+          o = min(x, x - span);
+        }
+      }
+      mark_run(segb, B, alim, step, mask);  // the last < 32 hits in plain order
+    }
+    if (stop) break;
+  }
+  const long long t1b = prof ? clock64() : 0;
+  (void)t1b;
+  // (ii-b) medium primes: prime i = R.skew + warp + nw*t, batches of 32 t's
+  for (uint32_t ib = R.skew + warp; ib < R.lanes; ib += 32u * nw) {
     const uint32_t i = ib + lane * nw;
     uint32_t pl = 0, jl = kNone;
     if (i < R.lanes) {
@@ -243,6 +292,7 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
     }
     if (stop) break;
   }
+  const long long t2 = prof ? clock64() : 0;
   // (iii) large primes: lane per prime (few hits each)
   for (uint32_t k = R.lanes + threadIdx.x; k < R.end; k += blockDim.x) {
     const uint32_t p = __ldg(primes + k);
@@ -255,6 +305,14 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
       mark(seg, j + 3u * p);
     }
     for (; j < valid; j += p) mark(seg, j);
+  }
+  if (prof) {  // per-warp busy cycles of the three regions (diagnostics only)
+    const long long t3 = clock64();
+    if ((threadIdx.x & 31u) == 0) {
+      atomicAdd(prof + 3, (unsigned long long)(t1 - t0));
+      atomicAdd(prof + 4, (unsigned long long)(t2 - t1));
+      atomicAdd(prof + 5, (unsigned long long)(t3 - t2));
+    }
   }
 }
 
@@ -316,7 +374,8 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, PrimeRegio
   R.start = min(ng_start, R.end);
   // primes with >= kSmallHits hits in a full segment: p * kSmallHits <= S
   R.mid = max(R.start, min(R.end, upper_bound_u32(P.primes, nb, P.seg_bits / kSmallHits)));
-  R.lanes = max(R.mid, min(R.end, upper_bound_u32(P.primes, nb, P.seg_bits / kLaneHits)));
+  R.skew = max(R.mid, min(R.end, upper_bound_u32(P.primes, nb, P.seg_bits / kSkewHits)));
+  R.lanes = max(R.skew, min(R.end, upper_bound_u32(P.primes, nb, P.seg_bits / kLaneHits)));
 }
 
 // ---------------------------------------------------------------------------
@@ -357,10 +416,13 @@ __global__ void __launch_bounds__(1024, 1) k_sieve(const SieveParams P) {
       valid = left < P.seg_bits ? (uint32_t)left : P.seg_bits;
       a = o0 + 2ull * bit0;
     }
+    const long long c0 = P.prof ? clock64() : 0;
     wheel_init<NG>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
-    mark_segment(seg, P.primes, P.recips, sR, a, valid);
+    const long long c1 = P.prof ? clock64() : 0;
+    mark_segment(seg, P.primes, P.recips, sR, a, valid, P.prof);
     __syncthreads();
+    const long long c2 = P.prof ? clock64() : 0;
     if (MODE == kBatch) {
       unsigned long long c = 0, sm = 0;
       epilogue<kCount>(seg, o0, bit0, valid, nullptr, 0, 0, c, sm);
@@ -383,6 +445,13 @@ __global__ void __launch_bounds__(1024, 1) k_sieve(const SieveParams P) {
     } else {
       epilogue<MODE>(seg, o0, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
       __syncthreads();
+    }
+    if (P.prof && threadIdx.x == 0) {  // CTA-level phase cycles (diagnostics only)
+      const long long c3 = clock64();
+      atomicAdd(P.prof + 0, (unsigned long long)(c1 - c0));
+      atomicAdd(P.prof + 1, (unsigned long long)(c2 - c1));
+      atomicAdd(P.prof + 2, (unsigned long long)(c3 - c2));
+      atomicAdd(P.prof + 6, 1ull);
     }
   }
   if (MODE == kBatch) return;

@@ -125,6 +125,7 @@ struct Ctx {
   DevBuf<sv::BatchItem> items;
   DevBuf<uint64_t> bres;
   uint64_t *h_res = nullptr;  // pinned [2]
+  unsigned long long *prof = nullptr;  // diagnostics: phase-cycle counters
   cudaStream_t stream() const { return user_set ? user : own; }
 };
 
@@ -132,7 +133,7 @@ Ctx g;
 
 void default_options(sieve_options &o) {
   memset(&o, 0, sizeof o);
-  o.segment_kb = 192;
+  o.segment_kb = 208;
   o.wheel = 37;
   o.ctas_per_sm = 0;
   o.threads = 1024;
@@ -277,6 +278,7 @@ sv::SieveParams params_for(const Plan &P, const uint32_t *primes, const uint64_t
   sp.add_two = P.two ? 1u : 0u;
   sp.done = g.done.p;
   sp.result = result;
+  sp.prof = g.prof;
   return sp;
 }
 
@@ -585,8 +587,8 @@ int sieve_set_options(const sieve_options *o) {
     for (int i = 0; i < 4; ++i)
       if (o->reserved[i]) return fail(SIEVE_EINVAL, "reserved option fields must be zero");
     if (o->segment_kb) {
-      if (o->segment_kb != 32 && o->segment_kb != 64 && o->segment_kb != 128 && o->segment_kb != 192)
-        return fail(SIEVE_EINVAL, "segment_kb %u not in {32,64,128,192}", o->segment_kb);
+      if (o->segment_kb % 16 != 0 || o->segment_kb > 208)
+        return fail(SIEVE_EINVAL, "segment_kb %u is not a multiple of 16 in [16, 208]", o->segment_kb);
       n.segment_kb = o->segment_kb;
     }
     if (o->wheel) {
@@ -632,5 +634,11 @@ void sieve_shutdown(void) {
 }
 
 uint64_t sieve_kernel_launches(void) { return g_launches.load(); }
+
+int sieve_debug_set_profile(uint64_t *dev_counters) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  g.prof = reinterpret_cast<unsigned long long *>(dev_counters);
+  return 0;
+}
 
 }  // extern "C"

@@ -44,13 +44,13 @@ def test_validation_before_device():
         sv.count(0, (1 << 48) + 1)
     assert e.value.code == -2
     with pytest.raises(sv.SieveError):
-        sv.set_options(segment_kb=48)
+        sv.set_options(segment_kb=40)
     with pytest.raises(sv.SieveError):
         sv.set_options(wheel=23)
     sv.set_options(segment_kb=64, wheel=61)
     assert sv.get_options()["segment_kb"] == 64
     sv.set_options()
-    assert sv.get_options() == {"segment_kb": 192, "wheel": 37, "ctas_per_sm": 0, "threads": 1024}
+    assert sv.get_options() == {"segment_kb": 208, "wheel": 37, "ctas_per_sm": 0, "threads": 1024}
 
 
 def test_no_cpu_fallback_without_gpu():

@@ -1,0 +1,25 @@
+"""Phase breakdown of the sieve kernel (diagnostics counters, not a bench number)."""
+import sys, json
+sys.path.insert(0, ".")
+import torch
+import paper_1205_4883_b200 as sv
+lo, hi = 2, 10**10 + 1
+for spec in sys.argv[1:] or [""]:
+    kw = dict(kv.split("=") for kv in spec.split(",") if kv)
+    kw = {k: int(v) for k, v in kw.items()}
+    sv.set_options(**kw)
+    sv.stats(lo, hi)
+    c = torch.zeros(8, dtype=torch.int64, device="cuda")
+    sv.debug_set_profile(c)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(); ev0.record(); r = sv.stats(lo, hi); ev1.record(); torch.cuda.synchronize()
+    sv.debug_set_profile(None)
+    v = c.cpu().tolist()
+    cta = v[0] + v[1] + v[2]
+    o = sv.get_options()
+    nw = o["threads"] // 32
+    print(json.dumps({"opts": o, "ms_with_prof": ev0.elapsed_time(ev1), "ok": r == (455052511, 2220822432581729238),
+          "segments": v[6], "cta_cycles_per_seg": cta / v[6],
+          "init%": 100 * v[0] / cta, "mark%": 100 * v[1] / cta, "epi%": 100 * v[2] / cta,
+          "warp_small_per_seg": v[3] / v[6] / nw, "warp_medium_per_seg": v[4] / v[6] / nw,
+          "warp_large_per_seg": v[5] / v[6] / nw, "mark_cta_per_seg": v[1] / v[6]}))
