@@ -150,6 +150,11 @@ uint64_t sieve_kernel_launches(void);
  * summed over warps), [6] segments.  NULL disables (the default). */
 int sieve_debug_set_profile(uint64_t *dev_counters);
 
+/* Diagnostics: flags for later launches.  1 = skip the marking step (A4/A5):
+ * wheel init + count/write-back only, to time the bitmap write-back stage in
+ * isolation.  Results are WRONG while set; 0 restores. */
+int sieve_debug_set_flags(uint32_t flags);
+
 #ifdef __cplusplus
 }
 #endif

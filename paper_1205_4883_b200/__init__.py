@@ -15,6 +15,7 @@ from ._abi import (  # noqa: F401
     bitmap_async,
     bitmap_words,
     count,
+    debug_set_flags,
     debug_set_profile,
     get_options,
     get_stream,

@@ -68,6 +68,7 @@ def lib():
             "sieve_shutdown": (None, []),
             "sieve_kernel_launches": (_u64, []),
             "sieve_debug_set_profile": (ctypes.c_int, [_p]),
+            "sieve_debug_set_flags": (ctypes.c_int, [ctypes.c_uint32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -205,6 +206,11 @@ def shutdown() -> None:
 def debug_set_profile(counters_t) -> None:
     """Diagnostics: phase-cycle counters (torch int64[8] CUDA tensor) or None."""
     _check(lib().sieve_debug_set_profile(_ptr(counters_t)))
+
+
+def debug_set_flags(flags: int) -> None:
+    """Diagnostics: 1 = skip marking (write-back-only timing; wrong results)."""
+    _check(lib().sieve_debug_set_flags(flags))
 
 
 def kernel_launches() -> int:

@@ -92,7 +92,13 @@ struct SieveParams {
   uint64_t *result;        // [2] count, sum mod 2^64 (batch: [2 * nintervals])
   const BatchItem *items;  // batch mode
   unsigned long long *prof;  // optional phase-cycle counters (diagnostics), [8]
+  uint32_t flags;            // diagnostics: kFlagSkipMarking
 };
+
+// Diagnostic flag: skip step A4/A5 (wheel init + count/write-back only), to
+// measure the bitmap write-back stage in isolation.  Results are then wrong
+// by design; never set on the product path.
+constexpr uint32_t kFlagSkipMarking = 1u;
 
 enum Mode { kCount = 0, kBitmap = 1, kBatch = 2 };
 

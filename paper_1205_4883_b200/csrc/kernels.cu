@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(1024, 1) k_sieve(const SieveParams P) {
     wheel_init<NG>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
-    mark_segment(seg, P.primes, P.recips, sR, a, valid, P.prof);
+    if (!(P.flags & kFlagSkipMarking)) mark_segment(seg, P.primes, P.recips, sR, a, valid, P.prof);
     __syncthreads();
     const long long c2 = P.prof ? clock64() : 0;
     if (MODE == kBatch) {

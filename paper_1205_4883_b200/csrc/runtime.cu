@@ -126,6 +126,7 @@ struct Ctx {
   DevBuf<uint64_t> bres;
   uint64_t *h_res = nullptr;  // pinned [2]
   unsigned long long *prof = nullptr;  // diagnostics: phase-cycle counters
+  uint32_t flags = 0;                  // diagnostics: sv::kFlagSkipMarking
   cudaStream_t stream() const { return user_set ? user : own; }
 };
 
@@ -279,6 +280,7 @@ sv::SieveParams params_for(const Plan &P, const uint32_t *primes, const uint64_t
   sp.done = g.done.p;
   sp.result = result;
   sp.prof = g.prof;
+  sp.flags = g.flags;
   return sp;
 }
 
@@ -634,6 +636,13 @@ void sieve_shutdown(void) {
 }
 
 uint64_t sieve_kernel_launches(void) { return g_launches.load(); }
+
+int sieve_debug_set_flags(uint32_t flags) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (flags & ~sv::kFlagSkipMarking) return fail(SIEVE_EINVAL, "unknown debug flags %u", flags);
+  g.flags = flags;
+  return 0;
+}
 
 int sieve_debug_set_profile(uint64_t *dev_counters) {
   std::lock_guard<std::mutex> lk(g.mu);

@@ -1,0 +1,143 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the multi-GPU host logic
+in paper_1205_4883_b200/dist.py: block partition, the packed base-prime
+broadcast, the u64-as-int64 all-reduce, and the LPT batch assignment with
+its all_gather reassembly.  The per-rank compute is injected (a CPU stand-in
+built on the oracle) because this container has no GPU; the CUDA backend is
+the default in the product path and is exercised by the -m gpu tests."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import inputs
+import oracle
+from paper_1205_4883_b200 import dist as D
+
+MASK64 = (1 << 64) - 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class OracleBackend:
+    """CPU stand-in for CudaBackend (test only): base primes from the
+    oracle, packed the same way; stats from the oracle, written into the
+    int64[2] result tensor as two's-complement u64."""
+
+    def base_capacity(self, r):
+        return max(32, len(oracle.base_primes(r)) + 8)
+
+    def base_primes(self, r, base):
+        pr = oracle.base_primes(r)
+        odd = pr[pr > 2].astype(np.int64)
+        base.primes[: odd.size] = torch.from_numpy(odd.astype(np.int32))
+        base.nbase[0] = int(odd.size)
+
+    def stats(self, a, b, base, result):
+        # the rank must see the broadcast primes: check them against its own copy
+        n = int(base.nbase[0])
+        got = base.primes[:n].numpy().astype(np.int64)
+        r = D.isqrt(b - 1) if b >= 2 else 0
+        mine = oracle.base_primes(r)
+        mine = mine[mine > 2]
+        assert np.array_equal(got[: mine.size], mine), "broadcast base primes differ"
+        c, s = oracle.stats(a, b, 1)
+        result[0] = D.u64_to_i64(c)
+        result[1] = D.u64_to_i64(s)
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = {}
+        be = OracleBackend()
+        cpu = torch.device("cpu")
+        for lo, hi in [(2, 10**6 + 1), (10**12, 10**12 + 3 * 10**5), (0, 0), (5, 6),
+                       (2**63 // 2**16, 2**63 // 2**16 + 10**5)]:
+            out[(lo, hi)] = D.stats(lo, hi, backend=be, device=cpu)
+        lo5, hi5 = inputs.config5_intervals(64)
+        c, s = D.batch(lo5, hi5, batch_fn=lambda a, b: oracle.batch(a, b, 1), device=cpu)
+        out["batch"] = (c.tolist(), s.tolist())
+        # u64 wrap across the all-reduce: two values whose sum wraps mod 2^64
+        t = torch.tensor([D.u64_to_i64((1 << 64) - 5 if rank == 0 else 9)], dtype=torch.int64)
+        dist.all_reduce(t)
+        out["wrap"] = D.i64_to_u64(int(t.item()))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_stats_batch_and_wrap():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1]
+    r = res[0]
+    for key, val in r.items():
+        if isinstance(key, tuple):
+            assert val == oracle.stats(*key), key
+    lo5, hi5 = inputs.config5_intervals(64)
+    oc, os_ = oracle.batch(lo5, hi5)
+    assert r["batch"] == (oc.tolist(), os_.tolist())
+    assert r["wrap"] == 4
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8, 13])
+def test_block_partition_tiles_range(G):
+    for lo, hi in [(2, 10**10 + 1), (0, 1), (0, 0), (7, 7 + 64 * 5 + 3), (10**12, 10**12 + 10**10),
+                   (123, 124), (1, 64 * 3)]:
+        blocks = [D.block_of(lo, hi, g, G) for g in range(G)]
+        assert blocks[0][0] == lo and blocks[-1][1] == hi
+        for (a0, b0), (a1, b1) in zip(blocks, blocks[1:]):
+            assert b0 == a1 and a0 <= b0
+        o0 = lo | 1
+        for a, _ in blocks[1:]:
+            if lo < a < hi:
+                assert (a - o0) % 64 == 0 and a % 2 == 1  # word-aligned odd boundary
+
+
+def test_block_partition_matches_survey_g2():
+    # config 3 at G=2 splits at 5000000003
+    assert D.block_of(2, 10**10 + 1, 0, 2) == (2, 5000000003)
+    assert D.block_of(2, 10**10 + 1, 1, 2) == (5000000003, 10**10 + 1)
+
+
+def test_block_additivity_small():
+    lo, hi = 10**9, 10**9 + 4 * 10**6 + 7
+    tot_c, tot_s = 0, 0
+    for g in range(5):
+        a, b = D.block_of(lo, hi, g, 5)
+        c, s = oracle.stats(a, b, 1)
+        tot_c += c
+        tot_s = (tot_s + s) & MASK64
+    assert (tot_c, tot_s) == oracle.stats(lo, hi)
+
+
+def test_lpt_assignment_properties():
+    lo, hi = inputs.config5_intervals()
+    cost = D.batch_cost(lo, hi)
+    for world in (1, 2, 8):
+        parts = D.lpt_assign(cost, world)
+        allidx = np.sort(np.concatenate(parts))
+        assert np.array_equal(allidx, np.arange(lo.size))
+        loads = np.array([cost[p].sum() for p in parts])
+        # LPT is within 4/3 of optimal; here the spread is tiny
+        assert loads.max() <= loads.mean() * 1.05 + cost.max()
