@@ -57,9 +57,10 @@ extern "C" {
 /* Tuning options (sieve_set_options).  Zero fields mean "default". */
 typedef struct sieve_options {
     uint32_t segment_kb;  /* shared-memory segment size in KiB: a multiple of 16 in [16, 208] (default 208) */
-    uint32_t wheel;       /* wheel bound w (pre-sieved primes 3..w): 19, 29, 37, 43, 53 or 61 (default 37) */
+    uint32_t wheel;       /* wheel bound w (pre-sieved primes 3..w): 11, 17, 23, 31, 41 or 47 (default 41);
+                             segment + wheel tables must fit 226 KiB of shared memory */
     uint32_t ctas_per_sm; /* resident CTAs per SM for the sieve kernel (default: occupancy maximum) */
-    uint32_t threads;     /* threads per CTA: 256, 512 or 1024 (default 1024) */
+    uint32_t threads;     /* threads per CTA: a multiple of 64 in [256, 768] (default 768) */
     uint32_t reserved[4]; /* must be zero */
 } sieve_options;
 

@@ -9,35 +9,38 @@ namespace sv {
 // ---------------------------------------------------------------------------
 // Wheel pre-sieve groups (step A3).  Group g is a set of small odd primes
 // whose product P_g is the period of their composite pattern on the odd-only
-// grid.  Table g holds bit i = 1 iff the odd integer 2i+1 is divisible by a
-// prime of the group, for i in [0, P_g + kTablePad) so that any 160-bit
-// window starting below P_g can be read without wrapping.
+// grid (bit i <-> odd integer 2i+1).  Because P_g is odd, the 32-bit words
+// of that pattern also repeat with period P_g words: word table g holds
+// WT_g[k] = bits 32k .. 32k+31 (mod P_g) of the pattern, k in [0, P_g), so a
+// segment word is ONE table load (its index advances by 1 per word, mod P_g).
 // ---------------------------------------------------------------------------
-constexpr int kMaxGroups = 7;
-constexpr uint32_t kTablePad = 160;
+constexpr int kMaxGroups = 6;
 __host__ __device__ constexpr uint32_t group_period(int g) {
-  return g == 0 ? 15015u   // 3*5*7*11*13
-       : g == 1 ? 323u     // 17*19
-       : g == 2 ? 667u     // 23*29
-       : g == 3 ? 1147u    // 31*37
-       : g == 4 ? 1763u    // 41*43
-       : g == 5 ? 2491u    // 47*53
-                : 3599u;   // 59*61
+  return g == 0 ? 1155u    // 3*5*7*11
+       : g == 1 ? 221u     // 13*17
+       : g == 2 ? 437u     // 19*23
+       : g == 3 ? 899u     // 29*31
+       : g == 4 ? 1517u    // 37*41
+                : 2021u;   // 43*47
 }
-__host__ __device__ constexpr uint32_t group_words(int g) {
-  return (group_period(g) + kTablePad + 31) / 32;
-}
+__host__ __device__ constexpr uint32_t group_words(int g) { return group_period(g); }
 __host__ __device__ constexpr uint32_t group_offset(int g) {
   return g == 0 ? 0u : group_offset(g - 1) + group_words(g - 1);
 }
 __host__ __device__ constexpr uint32_t tables_words(int ng) { return group_offset(ng); }
+// 32^-1 mod P (P odd): the word index of the word starting at pattern bit i is i * inv32
+__host__ __device__ constexpr uint32_t inv32_mod(uint32_t P) {
+  uint32_t x = 1;
+  while ((32ull * x) % P != 1) ++x;
+  return x;
+}
 // largest prime covered by the first ng groups (the wheel bound w)
 __host__ __device__ constexpr uint32_t wheel_bound(int ng) {
-  return ng == 1 ? 13u : ng == 2 ? 19u : ng == 3 ? 29u : ng == 4 ? 37u : ng == 5 ? 43u : ng == 6 ? 53u : 61u;
+  return ng == 1 ? 11u : ng == 2 ? 17u : ng == 3 ? 23u : ng == 4 ? 31u : ng == 5 ? 41u : 47u;
 }
 // number of odd primes <= wheel_bound(ng): index of the first marking prime
 __host__ __device__ constexpr uint32_t wheel_nprimes(int ng) {
-  return ng == 1 ? 5u : ng == 2 ? 7u : ng == 3 ? 9u : ng == 4 ? 11u : ng == 5 ? 13u : ng == 6 ? 15u : 17u;
+  return ng == 1 ? 4u : ng == 2 ? 6u : ng == 3 ? 8u : ng == 4 ? 10u : ng == 5 ? 12u : 14u;
 }
 // bit n set iff n is an odd prime <= 61
 constexpr uint64_t kOddPrimesBelow64 =
@@ -62,6 +65,12 @@ constexpr uint32_t kSkewHits = SIEVE_SKEW_HITS;
 #define SIEVE_LANE_HITS 128
 #endif
 constexpr uint32_t kLaneHits = SIEVE_LANE_HITS;
+
+// launch bound of the sieve kernel (threads per CTA); the runtime never
+// launches more (sieve_options.threads is clamped to it)
+#ifndef SIEVE_MAX_THREADS
+#define SIEVE_MAX_THREADS 768
+#endif
 
 // One work item of the batch kernel (step A10): one segment of one interval.
 struct BatchItem {

@@ -83,17 +83,18 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // A3: wheel pre-sieve of one segment into seg (composite = 1), plus the
 // fix-ups (1 is not prime; wheel primes in range are prime) and the tail
 // (slots >= valid are set composite).  Thread t builds words t, t+nt, ...:
-// the 32 lanes of a warp read 32 consecutive table words (conflict-free) and
-// funnel-shift each window into place.  Words up to the end of the last quad
-// are written so that the epilogue can read whole uint4 quads.
+// per group one load of the word table (the 32 lanes of a warp read 32
+// consecutive table words: conflict-free) and an OR.  Words up to the end of
+// the last quad are written so that the epilogue can read whole uint4 quads.
 template <int G>
 struct WheelGroup {
   static constexpr uint32_t P = group_period(G);
   static constexpr uint32_t OFF = group_offset(G);
+  static constexpr uint32_t INV32 = inv32_mod(group_period(G));
 };
 
-// OR the window of groups G..NG-1 for the current word and advance their
-// table indices (compile-time recursion: every modulus is a constant).
+// OR the table words of groups G..NG-1 for the current segment word and
+// advance their indices by nt words (compile-time recursion: constant moduli).
 template <int G, int NG>
 __device__ __forceinline__ uint32_t wheel_word(const uint32_t *tab, uint32_t (&ig)[NG],
                                                const uint32_t (&dg)[NG]) {
@@ -101,21 +102,23 @@ __device__ __forceinline__ uint32_t wheel_word(const uint32_t *tab, uint32_t (&i
     return 0u;
   } else {
     constexpr uint32_t P = WheelGroup<G>::P;
-    const uint32_t *t = tab + WheelGroup<G>::OFF + (ig[G] >> 5);
-    const uint32_t v = __funnelshift_r(t[0], t[1], ig[G] & 31u);
+    const uint32_t v = tab[WheelGroup<G>::OFF + ig[G]];
     const uint32_t x = ig[G] + dg[G];
     ig[G] = min(x, x - P);  // x < 2P: x - P wraps above x when x < P
     return v | wheel_word<G + 1, NG>(tab, ig, dg);
   }
 }
 
+// word index of segment word `tid`: (base * 32^-1 + tid) mod P, base = the
+// pattern bit of the segment's first slot
 template <int G, int NG>
 __device__ __forceinline__ void wheel_setup(uint32_t (&ig)[NG], uint32_t (&dg)[NG], uint64_t base,
                                             uint32_t tid, uint32_t nt) {
   if constexpr (G < NG) {
     constexpr uint32_t P = WheelGroup<G>::P;
-    ig[G] = (uint32_t)((base % P + (32u * tid) % P) % P);
-    dg[G] = (32u * nt) % P;
+    const uint32_t c0 = (uint32_t)((base % P) * WheelGroup<G>::INV32 % P);
+    ig[G] = (c0 + tid % P) % P;
+    dg[G] = nt % P;
     wheel_setup<G + 1, NG>(ig, dg, base, tid, nt);
   }
 }
@@ -208,6 +211,8 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
   const uint32_t vw = valid >> 5, vb = valid & 31u;
 
   // (i) small primes
+  const uint32_t c32 = 32u % nw;
+  uint32_t rot = (32u * R.start) % nw;
   for (uint32_t ib = R.start; ib < R.mid; ib += 32) {
     const uint32_t i = ib + lane;
     uint32_t pl = 0, jl = kNone;
@@ -220,7 +225,12 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
       const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
       const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
       if (j0 == kNone) break;  // p^2 past the segment, and so for every later prime
-      for (uint32_t r = warp; r < 32u; r += nw) {
+      // (prime, residue) units are dealt round robin over the warps:
+      // unit 32 i + r goes to warp (32 i + r) mod nw, rot = 32 i mod nw
+      const uint32_t r0 = warp >= rot ? warp - rot : warp + nw - rot;
+      rot += c32;
+      if (rot >= nw) rot -= nw;
+      for (uint32_t r = r0; r < 32u; r += nw) {
         const uint32_t jr = j0 + r * p;  // first hit of residue class r
         if (jr >= valid) break;
         const uint32_t bit = jr & 31u;
@@ -253,17 +263,24 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
       const uint32_t alim = (vw + (bit < vb ? 1u : 0u)) << 2;
       const uint32_t step = 4u * p, span = 128u * p;
       const uint32_t pinv = p * (2u - p * p);     // p^-1 mod 32 (Newton step from p^-1 = p mod 8)
-      uint32_t o = (((lane - w) * pinv) & 31u) * step;
       uint32_t B = w << 2;
       const uint32_t nh = B < alim ? (alim - B + step - 1u) / step : 0u;  // hits of this class
       const uint32_t full = nh >> 5;  // lanes differ by at most one chunk
-      for (uint32_t c = 0; c < full; ++c, B += span) {
+      if (full) {
+        // the 32 rotated byte offsets of a round, computed once per prime
+        uint32_t off[32];
+        off[0] = (((lane - w) * pinv) & 31u) * step;
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          atomicOr(reinterpret_cast<uint32_t *>(segb + B + o), mask);
-          const uint32_t x = o + step;
-          o = min(x, x - span);
+        for (int t = 1; t < 32; ++t) {
+          const uint32_t x = off[t - 1] + step;
+          off[t] = min(x, x - span);
         }
+        char *base = segb + B;
+        for (uint32_t c = 0; c < full; ++c, base += span) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) atomicOr(reinterpret_cast<uint32_t *>(base + off[t]), mask);
+        }
+        B += full * span;
       }
       mark_run(segb, B, alim, step, mask);  // the last < 32 hits in plain order
     }
@@ -317,37 +334,73 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
 }
 
 // A6/A7: count, sum and (bitmap mode) write-back of one segment.
+//
+// Sum of the primes of the segment = C*a + 2*J, where a is the segment's
+// first odd integer, C the number of set (prime) bits and J the sum of their
+// bit positions j = 128 q + 32 x + b (quad q, word x, bit b).  Per quad the
+// thread needs the quad's popcount (for C and 128 q c_q) and the word
+// popcounts (for 32 x); the bit-position part sum_b b * n_b is accumulated
+// without popcounts in carry-save bit planes (Harley-Seal adder tree: plane
+// k holds bit k of the per-position count n_b), and read once per segment.
+__device__ __forceinline__ void csa(uint32_t &carry, uint32_t &sum, uint32_t a, uint32_t b,
+                                    uint32_t c) {
+  const uint32_t u = a ^ b;
+  carry = (a & b) | (u & c);
+  sum = u ^ c;
+}
+
 template <int MODE>
-__device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t o0, uint64_t bit0,
+__device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64_t bit0,
                                          uint32_t valid, uint32_t *out, uint64_t out_words,
                                          uint32_t vec4, unsigned long long &cnt,
                                          unsigned long long &sum) {
   const uint32_t nq = (valid + 127u) >> 7;
   const uint4 *seg4 = reinterpret_cast<const uint4 *>(seg);
   const uint64_t w0 = bit0 >> 5;  // first word of the segment in the call's grid
-  for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+  // planes of per-bit-position counts (counts < 256 for <= 63 quads per thread)
+  uint32_t ones = 0, twos = 0, fours = 0, p8 = 0, p16 = 0, p32 = 0, p64 = 0, p128 = 0;
+  uint32_t C = 0, X = 0, Q = 0;  // count, sum of 32x over set bits / 32, sum of k c_k
+  uint32_t k = 0;
+  for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x, ++k) {
     const uint4 v = seg4[q];
-    const uint32_t w[4] = {~v.x, ~v.y, ~v.z, ~v.w};
-    const uint64_t gw = w0 + 4ull * q;
-    uint32_t c4 = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t c = __popc(w[k]);
-      c4 += c;
-      // primes o0 + 64*(gw+k) + 2b for the set bits b
-      sum += (unsigned long long)c * (o0 + 64ull * (gw + k)) + 2ull * bit_index_sum(w[k]);
-    }
-    cnt += c4;
+    const uint32_t x0 = ~v.x, x1 = ~v.y, x2 = ~v.z, x3 = ~v.w;
+    const uint32_t c0 = __popc(x0), c1 = __popc(x1), c2 = __popc(x2), c3 = __popc(x3);
+    const uint32_t cq = c0 + c1 + c2 + c3;
+    C += cq;
+    Q += k * cq;
+    X += c1 + 2u * c2 + 3u * c3;
+    uint32_t tA, tB, fA;
+    csa(tA, ones, ones, x0, x1);
+    csa(tB, ones, ones, x2, x3);
+    csa(fA, twos, twos, tA, tB);
+    uint32_t cy = fours & fA;  // half-adder chain for the weight-4 carries
+    fours ^= fA;
+    uint32_t cz = p8 & cy; p8 ^= cy;
+    cy = p16 & cz; p16 ^= cz;
+    cz = p32 & cy; p32 ^= cy;
+    cy = p64 & cz; p64 ^= cz;
+    p128 ^= cy;
     if (MODE == kBitmap) {
+      const uint64_t gw = w0 + 4ull * q;
       if (vec4 && gw + 4 <= out_words) {
-        reinterpret_cast<uint4 *>(out)[gw >> 2] = make_uint4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<uint4 *>(out)[gw >> 2] = make_uint4(x0, x1, x2, x3);
       } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (gw + k < out_words) out[gw + k] = w[k];
+        if (gw < out_words) out[gw] = x0;
+        if (gw + 1 < out_words) out[gw + 1] = x1;
+        if (gw + 2 < out_words) out[gw + 2] = x2;
+        if (gw + 3 < out_words) out[gw + 3] = x3;
       }
     }
   }
+  // sum of bit positions b over all set bits = sum_k 2^k bit_index_sum(plane_k)
+  const uint32_t B = bit_index_sum(ones) + 2u * bit_index_sum(twos) + 4u * bit_index_sum(fours) +
+                     8u * bit_index_sum(p8) + 16u * bit_index_sum(p16) + 32u * bit_index_sum(p32) +
+                     64u * bit_index_sum(p64) + 128u * bit_index_sum(p128);
+  // sum of 128 q over set bits, q = tid + k nt
+  const uint64_t Jq = 128ull * ((uint64_t)threadIdx.x * C + (uint64_t)blockDim.x * Q);
+  const uint64_t J = Jq + 32ull * X + B;
+  cnt += C;
+  sum += (unsigned long long)C * a + 2ull * J;
 }
 
 // block-wide sum of two u64 values; result valid in thread 0
@@ -367,15 +420,50 @@ __device__ __forceinline__ void block_sum2(unsigned long long &x, unsigned long 
   }
 }
 
-__device__ __forceinline__ void compute_regions(const SieveParams &P, PrimeRegions &R,
-                                                uint32_t ng_start) {
+// First index with v[idx] > x, by one warp: 32-ary search (each round the
+// 32 lanes sample 32 evenly spaced entries; a ballot of "<= x" narrows the
+// interval 32-fold), so a search over 2^18 primes costs ~4 dependent loads.
+__device__ __forceinline__ uint32_t warp_upper_bound(const uint32_t *v, uint32_t n, uint64_t x) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32u) {
+    const uint32_t step = (hi - lo + 31u) / 32u;
+    const uint32_t idx = lo + lane * step;
+    const bool le = idx < hi && (uint64_t)__ldg(v + idx) <= x;
+    const uint32_t c = __popc(__ballot_sync(0xffffffffu, le));  // sampled prefix <= x
+    if (c == 0) return lo;
+    const uint32_t nlo = lo + (c - 1u) * step + 1u;
+    hi = min(hi, lo + c * step);
+    lo = nlo;
+  }
+  const uint32_t idx = lo + lane;
+  const bool le = idx < hi && (uint64_t)__ldg(v + idx) <= x;
+  return lo + __popc(__ballot_sync(0xffffffffu, le));
+}
+
+// Region boundaries (indices into primes[]): warps 0..3 search in parallel,
+// then thread 0 clamps.  Must be called by the whole CTA (contains a barrier
+// before the clamp; the caller syncs after).
+__device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r, PrimeRegions &R,
+                                                uint32_t *scratch, uint32_t ng_start,
+                                                bool only_end) {
+  const uint32_t warp = threadIdx.x >> 5;
   const uint32_t nb = *P.nbase;
-  R.end = upper_bound_u32(P.primes, nb, P.r);
-  R.start = min(ng_start, R.end);
-  // primes with >= kSmallHits hits in a full segment: p * kSmallHits <= S
-  R.mid = max(R.start, min(R.end, upper_bound_u32(P.primes, nb, P.seg_bits / kSmallHits)));
-  R.skew = max(R.mid, min(R.end, upper_bound_u32(P.primes, nb, P.seg_bits / kSkewHits)));
-  R.lanes = max(R.skew, min(R.end, upper_bound_u32(P.primes, nb, P.seg_bits / kLaneHits)));
+  if (warp < (only_end ? 1u : 4u)) {
+    const uint64_t x = warp == 0 ? (uint64_t)r
+                     : warp == 1 ? P.seg_bits / kSmallHits
+                     : warp == 2 ? P.seg_bits / kSkewHits : P.seg_bits / kLaneHits;
+    const uint32_t u = warp_upper_bound(P.primes, nb, x);
+    if ((threadIdx.x & 31u) == 0) scratch[warp] = u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    R.end = scratch[0];
+    R.start = min(ng_start, R.end);
+    R.mid = max(R.start, min(R.end, scratch[1]));
+    R.skew = max(R.mid, min(R.end, scratch[2]));
+    R.lanes = max(R.skew, min(R.end, scratch[3]));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -385,16 +473,17 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, PrimeRegio
 // CTA ever reach HBM.
 // ---------------------------------------------------------------------------
 template <int NG, int MODE>
-__global__ void __launch_bounds__(1024, 1) k_sieve(const SieveParams P) {
+__global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t *seg = smem;
   uint32_t *tab = smem + P.seg_bits / 32;
   __shared__ unsigned long long red[64];
   __shared__ PrimeRegions sR;
   __shared__ uint32_t s_last;
+  __shared__ uint32_t s_ub[4];
 
   for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
-  if (threadIdx.x == 0 && MODE != kBatch) compute_regions(P, sR, wheel_nprimes(NG));
+  compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
   __syncthreads();
 
   unsigned long long cnt = 0, sum = 0;
@@ -404,11 +493,7 @@ __global__ void __launch_bounds__(1024, 1) k_sieve(const SieveParams P) {
     if (MODE == kBatch) {
       const BatchItem it = P.items[s];
       a = it.a; valid = it.valid; o0 = it.a; bit0 = 0;
-      if (threadIdx.x == 0) {
-        SieveParams Q = P;
-        Q.r = it.r;
-        compute_regions(Q, sR, wheel_nprimes(NG));
-      }
+      compute_regions(P, it.r, sR, s_ub, wheel_nprimes(NG), true);
     } else {
       o0 = P.o0;
       bit0 = s * (uint64_t)P.seg_bits;
@@ -425,7 +510,7 @@ __global__ void __launch_bounds__(1024, 1) k_sieve(const SieveParams P) {
     const long long c2 = P.prof ? clock64() : 0;
     if (MODE == kBatch) {
       unsigned long long c = 0, sm = 0;
-      epilogue<kCount>(seg, o0, bit0, valid, nullptr, 0, 0, c, sm);
+      epilogue<kCount>(seg, a, bit0, valid, nullptr, 0, 0, c, sm);
       block_sum2(c, sm, red);
       if (threadIdx.x == 0) {
         const uint32_t iv = P.items[s].interval;
@@ -435,7 +520,7 @@ __global__ void __launch_bounds__(1024, 1) k_sieve(const SieveParams P) {
       __syncthreads();
     } else if (MODE == kBitmap && P.seg_counts) {
       unsigned long long c = 0, sm = 0;
-      epilogue<kBitmap>(seg, o0, bit0, valid, P.out, P.out_words, P.out_vec4, c, sm);
+      epilogue<kBitmap>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, c, sm);
       cnt += c;
       sum += sm;
       unsigned long long c2 = c, z = 0;
@@ -443,7 +528,7 @@ __global__ void __launch_bounds__(1024, 1) k_sieve(const SieveParams P) {
       if (threadIdx.x == 0) P.seg_counts[s] = (uint32_t)c2;
       __syncthreads();
     } else {
-      epilogue<MODE>(seg, o0, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
+      epilogue<MODE>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
       __syncthreads();
     }
     if (P.prof && threadIdx.x == 0) {  // CTA-level phase cycles (diagnostics only)
@@ -535,18 +620,20 @@ __global__ void __launch_bounds__(1024, 1) k_base_primes(uint32_t r, uint32_t rs
     const uint32_t nwords = (nbits + 31) / 32;
     for (uint32_t w = tid; w < nwords; w += nt) bm[w] = 0;
     __syncthreads();
-    const uint64_t a = 2ull * i0 + 1;  // odd integer of bit 0
-    const uint64_t e = a + 2ull * nbits;
-    for (uint32_t k = warp; k < nsp; k += nw) {
+    const uint32_t a = 2u * i0 + 1u;  // odd integer of bit 0 (r <= 2^24: 32-bit math)
+    const uint32_t e = a + 2u * nbits;
+    // every thread of the CTA on one small prime at a time (the tiny primes
+    // carry most of the marks; a warp per prime would serialise on q = 3)
+    for (uint32_t k = 0; k < nsp; ++k) {
       const uint32_t q = sp[k];
-      const uint64_t qq = (uint64_t)q * q;
+      const uint32_t qq = q * q;
       if (qq >= e) break;
-      uint64_t m = qq;
+      uint32_t m = qq;
       if (m < a) {
-        m = ((a + q - 1) / q) * q;
-        if (!(m & 1ull)) m += q;
+        m = ((a + q - 1u) / q) * q;
+        if (!(m & 1u)) m += q;
       }
-      for (uint64_t j = (m - a) / 2 + (uint64_t)lane * q; j < nbits; j += 32ull * q)
+      for (uint32_t j = (m - a) / 2u + tid * q; j < nbits; j += nt * q)
         atomicOr(&bm[j >> 5], 1u << (j & 31));
     }
     __syncthreads();
@@ -697,12 +784,12 @@ template <int MODE>
 static cudaError_t launch_m(int ng, const SieveParams &p, int grid, int threads, size_t smem,
                             cudaStream_t s) {
   switch (ng) {
+    case 1: return launch_t<1, MODE>(p, grid, threads, smem, s);
     case 2: return launch_t<2, MODE>(p, grid, threads, smem, s);
     case 3: return launch_t<3, MODE>(p, grid, threads, smem, s);
     case 4: return launch_t<4, MODE>(p, grid, threads, smem, s);
     case 5: return launch_t<5, MODE>(p, grid, threads, smem, s);
     case 6: return launch_t<6, MODE>(p, grid, threads, smem, s);
-    case 7: return launch_t<7, MODE>(p, grid, threads, smem, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -727,12 +814,12 @@ static cudaError_t set_attr_ng(size_t smem) {
 
 cudaError_t set_sieve_smem_limits(size_t smem) {
   cudaError_t e;
+  if ((e = set_attr_ng<1>(smem))) return e;
   if ((e = set_attr_ng<2>(smem))) return e;
   if ((e = set_attr_ng<3>(smem))) return e;
   if ((e = set_attr_ng<4>(smem))) return e;
   if ((e = set_attr_ng<5>(smem))) return e;
   if ((e = set_attr_ng<6>(smem))) return e;
-  if ((e = set_attr_ng<7>(smem))) return e;
   return cudaFuncSetAttribute(k_base_primes, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(kBaseChunkBits / 8));
 }
@@ -747,7 +834,7 @@ static int occ_t(int threads, size_t smem) {
 
 int sieve_max_ctas_per_sm(int ng, int mode, int threads, size_t smem) {
   (void)ng; (void)mode;
-  return occ_t<5, kCount>(threads, smem);
+  return occ_t<4, kCount>(threads, smem);
 }
 
 cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64_t *recips,

@@ -131,42 +131,45 @@ struct Ctx {
 };
 
 Ctx g;
+constexpr size_t kMaxDynSmem = 227 * 1024 - 1024;  // per-block limit minus static shared memory
 
 void default_options(sieve_options &o) {
   memset(&o, 0, sizeof o);
   o.segment_kb = 208;
-  o.wheel = 37;
+  o.wheel = 41;
   o.ctas_per_sm = 0;
-  o.threads = 1024;
+  o.threads = SIEVE_MAX_THREADS;
 }
 
 int ng_for_wheel(uint32_t w) {
   switch (w) {
-    case 19: return 2;
-    case 29: return 3;
-    case 37: return 4;
-    case 43: return 5;
-    case 53: return 6;
-    case 61: return 7;
+    case 11: return 1;
+    case 17: return 2;
+    case 23: return 3;
+    case 31: return 4;
+    case 41: return 5;
+    case 47: return 6;
     default: return -1;
   }
 }
 
-// wheel table g: bit i set iff 2i+1 is divisible by a prime of group g
+// word table g: WT[k] bit b = 1 iff 2i+1 is divisible by a prime of group g,
+// i = (32k + b) mod P_g
 void build_tables(std::vector<uint32_t> &t) {
-  static const uint32_t groups[sv::kMaxGroups][5] = {
-      {3, 5, 7, 11, 13}, {17, 19, 0, 0, 0}, {23, 29, 0, 0, 0}, {31, 37, 0, 0, 0},
-      {41, 43, 0, 0, 0}, {47, 53, 0, 0, 0}, {59, 61, 0, 0, 0}};
+  static const uint32_t groups[sv::kMaxGroups][4] = {
+      {3, 5, 7, 11}, {13, 17, 0, 0}, {19, 23, 0, 0}, {29, 31, 0, 0}, {37, 41, 0, 0}, {43, 47, 0, 0}};
   t.assign(sv::tables_words(sv::kMaxGroups), 0u);
   for (int g = 0; g < sv::kMaxGroups; ++g) {
-    const uint32_t nbits = sv::group_words(g) * 32;
+    const uint32_t P = sv::group_period(g);
     uint32_t *w = t.data() + sv::group_offset(g);
-    for (uint32_t i = 0; i < nbits; ++i) {
-      const uint64_t n = 2ull * i + 1;
-      bool hit = false;
-      for (int k = 0; k < 5 && groups[g][k]; ++k) hit |= (n % groups[g][k]) == 0;
-      if (hit) w[i >> 5] |= 1u << (i & 31);
-    }
+    for (uint32_t k = 0; k < P; ++k)
+      for (uint32_t b = 0; b < 32; ++b) {
+        const uint64_t i = (32ull * k + b) % P;
+        const uint64_t n = 2 * i + 1;
+        bool hit = false;
+        for (int q = 0; q < 4 && groups[g][q]; ++q) hit |= (n % groups[g][q]) == 0;
+        if (hit) w[k] |= 1u << b;
+      }
   }
 }
 
@@ -194,7 +197,10 @@ int ensure_ready() {
 }
 
 size_t seg_bits() { return (size_t)g.opt.segment_kb * 8192; }
-size_t sieve_smem() { return seg_bits() / 8 + sv::tables_words(sv::kMaxGroups) * 4; }
+size_t smem_for(uint32_t segment_kb, uint32_t wheel) {
+  return (size_t)segment_kb * 1024 + sv::tables_words(ng_for_wheel(wheel)) * 4;
+}
+size_t sieve_smem() { return smem_for(g.opt.segment_kb, g.opt.wheel); }
 
 int ensure_smem_attr() {
   const size_t sm = sieve_smem();
@@ -595,15 +601,19 @@ int sieve_set_options(const sieve_options *o) {
     }
     if (o->wheel) {
       if (ng_for_wheel(o->wheel) < 0)
-        return fail(SIEVE_EINVAL, "wheel %u not in {19,29,37,43,53,61}", o->wheel);
+        return fail(SIEVE_EINVAL, "wheel %u not in {11,17,23,31,41,47}", o->wheel);
       n.wheel = o->wheel;
     }
     if (o->threads) {
-      if (o->threads != 256 && o->threads != 512 && o->threads != 1024)
-        return fail(SIEVE_EINVAL, "threads %u not in {256,512,1024}", o->threads);
+      if (o->threads % 64 != 0 || o->threads < 256 || o->threads > SIEVE_MAX_THREADS)
+        return fail(SIEVE_EINVAL, "threads %u is not a multiple of 64 in [256, %d]", o->threads,
+                    SIEVE_MAX_THREADS);
       n.threads = o->threads;
     }
     if (o->ctas_per_sm > 32) return fail(SIEVE_EINVAL, "ctas_per_sm %u > 32", o->ctas_per_sm);
+    if (smem_for(n.segment_kb, n.wheel) > kMaxDynSmem)
+      return fail(SIEVE_EINVAL, "segment_kb %u with wheel %u needs %zu bytes of shared memory (> %zu)",
+                  n.segment_kb, n.wheel, smem_for(n.segment_kb, n.wheel), kMaxDynSmem);
     n.ctas_per_sm = o->ctas_per_sm;
   }
   g.opt = n;

@@ -46,11 +46,13 @@ def test_validation_before_device():
     with pytest.raises(sv.SieveError):
         sv.set_options(segment_kb=40)
     with pytest.raises(sv.SieveError):
-        sv.set_options(wheel=23)
-    sv.set_options(segment_kb=64, wheel=61)
+        sv.set_options(wheel=19)
+    sv.set_options(segment_kb=64, wheel=47)
+    with pytest.raises(sv.SieveError):
+        sv.set_options(segment_kb=208, wheel=47)  # 208 KiB + 25 KiB of tables > 226 KiB
     assert sv.get_options()["segment_kb"] == 64
     sv.set_options()
-    assert sv.get_options() == {"segment_kb": 208, "wheel": 37, "ctas_per_sm": 0, "threads": 1024}
+    assert sv.get_options() == {"segment_kb": 208, "wheel": 41, "ctas_per_sm": 0, "threads": 768}
 
 
 def test_no_cpu_fallback_without_gpu():

@@ -106,8 +106,10 @@ def test_random_intervals_stats(seed):
 
 
 @pytest.mark.parametrize("seg_kb", [32, 64, 128, 192])
-@pytest.mark.parametrize("wheel", [19, 37, 61])
+@pytest.mark.parametrize("wheel", [11, 17, 23, 31, 41, 47])
 def test_bitmap_multi_segment_ragged(seg_kb, wheel):
+    if seg_kb == 192 and wheel == 47:
+        pytest.skip("192 KiB + 25 KiB of wheel tables exceed shared memory")
     sv.set_options(segment_kb=seg_kb, wheel=wheel)
     for lo, hi in [(0, 3 * 10**7 + 17), (10**12 + 3, 10**12 + 2 * 10**7 + 1), (999_999_999_989, 1_000_040_000_000)]:
         bm, c = sv.bitmap(lo, hi)
@@ -117,7 +119,7 @@ def test_bitmap_multi_segment_ragged(seg_kb, wheel):
         assert sv.stats(lo, hi) == (oc, os_)
 
 
-@pytest.mark.parametrize("threads", [256, 512, 1024])
+@pytest.mark.parametrize("threads", [256, 512, 768])
 def test_thread_and_occupancy_invariance(threads):
     sv.set_options(threads=threads, segment_kb=64, ctas_per_sm=2)
     lo, hi = 10**11, 10**11 + 5 * 10**7 + 3

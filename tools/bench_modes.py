@@ -60,8 +60,11 @@ def emit(d):
     print(json.dumps(d), flush=True)
 
 
-def config2(seg_kb):
-    sv.set_options(segment_kb=seg_kb)
+def config2(opts):
+    if isinstance(opts, int):
+        opts = {"segment_kb": opts}
+    sv.set_options(**opts)
+    seg_kb = sv.get_options()
     lo, hi = inputs.CONFIG2
     r, b = base_for(hi)
     words = sv.bitmap_words(lo, hi)
@@ -133,12 +136,17 @@ def config5():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["1", "2", "4", "5"]
+    which = [a for a in sys.argv[1:] if "=" not in a] or ["1", "2", "4", "5"]
     if "1" in which:
         config1()
     if "2" in which:
-        for kb in (32, 64, 128, 192, 208):
-            config2(kb)
+        specs = [a for a in sys.argv[1:] if "=" in a]
+        if specs:
+            for spec in specs:
+                config2({k: int(v) for k, v in (kv.split("=") for kv in spec.split(","))})
+        else:
+            for kb in (32, 64, 128, 192, 208):
+                config2(kb)
     if "4" in which:
         for kb in (32, 208):
             config4(kb)
