@@ -53,7 +53,7 @@ constexpr uint64_t kOddPrimesBelow64 =
 // atomics); primes with kSkewHits <= K < kSmallHits one per warp, one residue
 // class per lane with rotated starts (conflict-free atomics).
 #ifndef SIEVE_SMALL_HITS
-#define SIEVE_SMALL_HITS 16384
+#define SIEVE_SMALL_HITS 32768
 #endif
 constexpr uint32_t kSmallHits = SIEVE_SMALL_HITS;
 #ifndef SIEVE_SKEW_HITS
