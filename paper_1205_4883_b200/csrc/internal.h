@@ -65,6 +65,11 @@ constexpr uint32_t kSkewHits = SIEVE_SKEW_HITS;
 #define SIEVE_LANE_HITS 128
 #endif
 constexpr uint32_t kLaneHits = SIEVE_LANE_HITS;
+// primes a thread handles at once in the lane-per-prime region (load ILP)
+#ifndef SIEVE_LARGE_ILP
+#define SIEVE_LARGE_ILP 4
+#endif
+constexpr int kLargeILP = SIEVE_LARGE_ILP;
 
 // launch bound of the sieve kernel (threads per CTA); the runtime never
 // launches more (sieve_options.threads is clamped to it)

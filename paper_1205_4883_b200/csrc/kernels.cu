@@ -41,18 +41,19 @@ __device__ __forceinline__ void mark(uint32_t *seg, uint32_t j) {
 // a mod p by Barrett reduction with recip = floor((2^64-1)/p): the quotient
 // estimate is floor(a/p) or one less, so one conditional subtraction is exact
 // for any a < 2^64.
+// Branch-free, so that the loads of p and recip issue together (an early
+// return on p^2 would make the recip load wait for the p load).
 __device__ __forceinline__ uint32_t first_hit(uint64_t a, uint64_t seg_end, uint32_t p,
                                               uint64_t recip) {
   const uint64_t pp = (uint64_t)p * p;
-  if (pp >= seg_end) return kNone;
   const uint64_t q = __umul64hi(a, recip);
   uint32_t r = (uint32_t)(a - q * (uint64_t)p);
-  if (r >= p) r -= p;
-  uint32_t d = r ? p - r : 0u;  // a + d == 0 (mod p)
-  if (d & 1u) d += p;           // a odd: the odd multiple is a + d with d even
+  r = min(r, r - p);              // r in [0, 2p) -> [0, p)
+  uint32_t d = r ? p - r : 0u;    // a + d == 0 (mod p)
+  d += (d & 1u) ? p : 0u;         // a odd: the odd multiple is a + d with d even
   uint32_t j = d >> 1;
-  if (a + 2ull * j < pp) j = (uint32_t)((pp - a) >> 1);
-  return j;
+  j = (a + 2ull * j < pp) ? (uint32_t)((pp - a) >> 1) : j;
+  return pp >= seg_end ? kNone : j;
 }
 
 __device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t *v, uint32_t n, uint64_t x) {
@@ -310,18 +311,37 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
     if (stop) break;
   }
   const long long t2 = prof ? clock64() : 0;
-  // (iii) large primes: lane per prime (few hits each)
-  for (uint32_t k = R.lanes + threadIdx.x; k < R.end; k += blockDim.x) {
-    const uint32_t p = __ldg(primes + k);
-    uint32_t j = first_hit(a, seg_end, p, __ldg(recips + k));
-    if (j == kNone) break;
-    for (; j + 3u * p < valid; j += 4u * p) {
-      mark(seg, j);
-      mark(seg, j + p);
-      mark(seg, j + 2u * p);
-      mark(seg, j + 3u * p);
+  // (iii) large primes: lane per prime (few hits each).  Each thread takes
+  // kLargeILP primes per iteration and issues all their loads and Barrett
+  // reductions before marking, so the L2 latency of the prime list overlaps.
+  for (uint32_t k0 = R.lanes + threadIdx.x; k0 < R.end; k0 += kLargeILP * blockDim.x) {
+    uint32_t pk[kLargeILP], jk[kLargeILP];
+    uint64_t rk[kLargeILP];
+#pragma unroll
+    for (int u = 0; u < kLargeILP; ++u) {  // all loads first (clamped index: no branch)
+      const uint32_t k = min(k0 + u * blockDim.x, R.end - 1u);
+      pk[u] = __ldg(primes + k);
+      rk[u] = __ldg(recips + k);
     }
-    for (; j < valid; j += p) mark(seg, j);
+#pragma unroll
+    for (int u = 0; u < kLargeILP; ++u) {
+      jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
+      if (k0 + u * blockDim.x >= R.end) jk[u] = kNone;
+    }
+    if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
+#pragma unroll
+    for (int u = 0; u < kLargeILP; ++u) {
+      const uint32_t p = pk[u];
+      uint32_t j = jk[u];
+      if (j == kNone) break;
+      for (; j + 3u * p < valid; j += 4u * p) {
+        mark(seg, j);
+        mark(seg, j + p);
+        mark(seg, j + 2u * p);
+        mark(seg, j + 3u * p);
+      }
+      for (; j < valid; j += p) mark(seg, j);
+    }
   }
   if (prof) {  // per-warp busy cycles of the three regions (diagnostics only)
     const long long t3 = clock64();
