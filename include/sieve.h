@@ -60,7 +60,7 @@ typedef struct sieve_options {
     uint32_t wheel;       /* wheel bound w (pre-sieved primes 3..w): 11, 17, 23, 31, 41 or 47 (default 41);
                              segment + wheel tables must fit 226 KiB of shared memory */
     uint32_t ctas_per_sm; /* resident CTAs per SM for the sieve kernel (default: occupancy maximum) */
-    uint32_t threads;     /* threads per CTA: a multiple of 64 in [256, 768] (default 768) */
+    uint32_t threads;     /* threads per CTA: a multiple of 64 in [256, 1024] (default 1024) */
     uint32_t reserved[4]; /* must be zero */
 } sieve_options;
 

@@ -7,12 +7,21 @@
 namespace sv {
 
 // ---------------------------------------------------------------------------
+// Segment layout in shared memory: BANK-TRANSPOSED.  Bit j of a segment
+// (odd slot j, integer a + 2j) lives in word T(j) = 32 (j >> 10) + (j & 31),
+// at bit position (j >> 5) & 31: every 1024-slot block is a 32x32 bit matrix
+// stored transposed, so the shared-memory bank of slot j is j mod 32.  For an
+// odd prime p, any 32 consecutive hits j0 + k p (or 32 consecutive residue
+// classes k mod 1024) then fall into 32 distinct banks: the marking atomics of
+// a warp that works on one prime never conflict.
+//
 // Wheel pre-sieve groups (step A3).  Group g is a set of small odd primes
 // whose product P_g is the period of their composite pattern on the odd-only
-// grid (bit i <-> odd integer 2i+1).  Because P_g is odd, the 32-bit words
-// of that pattern also repeat with period P_g words: word table g holds
-// WT_g[k] = bits 32k .. 32k+31 (mod P_g) of the pattern, k in [0, P_g), so a
-// segment word is ONE table load (its index advances by 1 per word, mod P_g).
+// grid (global odd index x <-> odd integer 2x+1).  Word table g holds, for
+// y in [0, P_g), TT_g[y] bit i = pattern_g[(y + 32 i) mod P_g]: the transposed
+// word of bank b in block B of a segment starting at global index X0 is
+// TT_g[(X0 + 1024 B + b) mod P_g] -- ONE table load per word, whose index
+// advances by a constant (mod P_g) from one word of a thread to the next.
 // ---------------------------------------------------------------------------
 constexpr int kMaxGroups = 6;
 __host__ __device__ constexpr uint32_t group_period(int g) {
@@ -28,12 +37,6 @@ __host__ __device__ constexpr uint32_t group_offset(int g) {
   return g == 0 ? 0u : group_offset(g - 1) + group_words(g - 1);
 }
 __host__ __device__ constexpr uint32_t tables_words(int ng) { return group_offset(ng); }
-// 32^-1 mod P (P odd): the word index of the word starting at pattern bit i is i * inv32
-__host__ __device__ constexpr uint32_t inv32_mod(uint32_t P) {
-  uint32_t x = 1;
-  while ((32ull * x) % P != 1) ++x;
-  return x;
-}
 // largest prime covered by the first ng groups (the wheel bound w)
 __host__ __device__ constexpr uint32_t wheel_bound(int ng) {
   return ng == 1 ? 11u : ng == 2 ? 17u : ng == 3 ? 23u : ng == 4 ? 31u : ng == 5 ? 41u : 47u;
@@ -48,33 +51,39 @@ constexpr uint64_t kOddPrimesBelow64 =
     (1ull << 19) | (1ull << 23) | (1ull << 29) | (1ull << 31) | (1ull << 37) | (1ull << 41) |
     (1ull << 43) | (1ull << 47) | (1ull << 53) | (1ull << 59) | (1ull << 61);
 
-// Marking-work partition (step A4): primes with at least kSmallHits hits per
-// segment are marked by residue class mod 32 across warps (conflict-free
-// atomics); primes with kSkewHits <= K < kSmallHits one per warp, one residue
-// class per lane with rotated starts (conflict-free atomics).
-#ifndef SIEVE_SMALL_HITS
-#define SIEVE_SMALL_HITS 32768
+// Marking-work partition (steps A4/A5) by K = S / p, the hits of prime p in a
+// full segment of S slots:
+//   K >= kUnitHits            : (prime, class group) units over all warps
+//   kClassHits <= K < kUnitHits: warp per prime, lanes walk residue classes
+//                                mod 1024 (constant mask and stride)
+//   kWarpHits <= K < kClassHits: warp per prime, lanes on consecutive hits
+//   K < kWarpHits             : lane per prime
+#ifndef SIEVE_UNIT_HITS
+#define SIEVE_UNIT_HITS 32768
 #endif
-constexpr uint32_t kSmallHits = SIEVE_SMALL_HITS;
-#ifndef SIEVE_SKEW_HITS
-#define SIEVE_SKEW_HITS 1024
+constexpr uint32_t kUnitHits = SIEVE_UNIT_HITS;
+#ifndef SIEVE_CLASS_HITS
+#define SIEVE_CLASS_HITS 16384
 #endif
-constexpr uint32_t kSkewHits = SIEVE_SKEW_HITS;
-// primes with fewer than kLaneHits hits per segment are marked lane-per-prime
-#ifndef SIEVE_LANE_HITS
-#define SIEVE_LANE_HITS 128
+constexpr uint32_t kClassHits = SIEVE_CLASS_HITS;
+#ifndef SIEVE_WARP_HITS
+#define SIEVE_WARP_HITS 256
 #endif
-constexpr uint32_t kLaneHits = SIEVE_LANE_HITS;
+constexpr uint32_t kWarpHits = SIEVE_WARP_HITS;
 // primes a thread handles at once in the lane-per-prime region (load ILP)
 #ifndef SIEVE_LARGE_ILP
-#define SIEVE_LARGE_ILP 4
+#define SIEVE_LARGE_ILP 2
 #endif
 constexpr int kLargeILP = SIEVE_LARGE_ILP;
+
+// alignment of the segment in shared memory (the runtime adds this many spare
+// bytes to the dynamic shared-memory size)
+constexpr uint32_t kSmemAlign = 128;
 
 // launch bound of the sieve kernel (threads per CTA); the runtime never
 // launches more (sieve_options.threads is clamped to it)
 #ifndef SIEVE_MAX_THREADS
-#define SIEVE_MAX_THREADS 768
+#define SIEVE_MAX_THREADS 1024
 #endif
 
 // One work item of the batch kernel (step A10): one segment of one interval.

@@ -7,8 +7,9 @@
 //                       base prime w < p <= r, starting at max(p^2, first
 //                       odd multiple >= segment start)  (PAPER.md:131,
 //                       "iteratively marking as composite the multiples of
-//                       each prime"; SPEC.md:158 start rule)
-//   A5  large primes  : primes with < kLaneHits hits per segment are marked
+//                       each prime"; SPEC.md:158 start rule), conflict-free
+//                       in the bank-transposed segment layout (internal.h)
+//   A5  large primes  : primes with < kWarpHits hits per segment are marked
 //                       lane-per-prime straight from their first hit, so a
 //                       segment a prime skips costs one Barrett reduction
 //   A6  count + sum   : popc of the inverted words, weighted popcs for the sum
@@ -18,7 +19,8 @@
 //
 // Bit j of a call's odd-only grid <-> the odd integer o0 + 2j (o0 = lo|1).
 // In shared memory a set bit means "composite" (the paper's marking); the
-// write-back inverts it so that the bitmap has 1 = prime (reading R5).
+// write-back inverts it so that the bitmap has 1 = prime (reading R5), and
+// transposes each 1024-slot block back to the natural bit order.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -31,11 +33,6 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 // ---------------------------------------------------------------------------
 // helpers
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void mark(uint32_t *seg, uint32_t j) {
-  // bit j of the segment: word j>>5, bit j&31 (SHF.L.W wraps the shift)
-  atomicOr(&seg[j >> 5], __funnelshift_l(0u, 1u, j));
-}
-
 // Offset (in odd slots from a) of the first odd multiple m of p with
 // m >= max(a, p*p); kNone when p*p >= seg_end.  a is odd, m = a + 2*j.
 // a mod p by Barrett reduction with recip = floor((2^64-1)/p): the quotient
@@ -78,24 +75,50 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 }
 
 // ---------------------------------------------------------------------------
-// Segment phases
+// Segment phases.  The segment is held in the bank-transposed layout of
+// internal.h: slot j <-> word 32 (j >> 10) + (j & 31), bit (j >> 5) & 31.
 // ---------------------------------------------------------------------------
+
+// shared-memory OR without return (ATOMS.OR RZ) at a 32-bit shared-window
+// byte address: the segment base is 128-byte aligned and kept in a register,
+// so that the address arithmetic below needs no generic->shared conversion
+__device__ __forceinline__ void red_or(uint32_t saddr, uint32_t mask) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(saddr), "r"(mask) : "memory");
+}
+
+// byte address (shared window) and bit mask of slot j in the transposed
+// segment from J = 4 j + 32 sb: (J >> 5) & ~127 | J & 127 as ONE lop3, and
+// 1 << ((J >> 7) & 31)
+__device__ __forceinline__ uint32_t j_addr(uint32_t J) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, 127, %2, 0xB8;" : "=r"(d) : "r"(J >> 5), "r"(J));  // (a & ~b) | (c & b)
+  return d;
+}
+__device__ __forceinline__ uint32_t j_mask(uint32_t J) { return __funnelshift_l(0u, 1u, J >> 7); }
+
+// byte offset and bit mask of slot j in the transposed segment
+__device__ __forceinline__ uint32_t t_addr(uint32_t j) {
+  return ((j >> 3) & ~127u) | ((j & 31u) << 2);
+}
+__device__ __forceinline__ uint32_t t_mask(uint32_t j) { return __funnelshift_l(0u, 1u, j >> 5); }
+__device__ __forceinline__ uint32_t rotl(uint32_t x, uint32_t s) { return __funnelshift_l(x, x, s); }
 
 // A3: wheel pre-sieve of one segment into seg (composite = 1), plus the
 // fix-ups (1 is not prime; wheel primes in range are prime) and the tail
-// (slots >= valid are set composite).  Thread t builds words t, t+nt, ...:
-// per group one load of the word table (the 32 lanes of a warp read 32
-// consecutive table words: conflict-free) and an OR.  Words up to the end of
-// the last quad are written so that the epilogue can read whole uint4 quads.
+// (slots >= valid are set composite).  Thread t builds words t, t+nt, ...;
+// word T (bank b = T & 31, block B = T >> 5) of group g is the table word
+// TT_g[(X0 + 1024 B + b) mod P_g]: the 32 lanes of a warp read 32 consecutive
+// table words (conflict-free), and the index of a thread advances by
+// 32 nt (mod P_g) per word.  Whole 1024-slot blocks are written, so that the
+// epilogue can read whole blocks.
 template <int G>
 struct WheelGroup {
   static constexpr uint32_t P = group_period(G);
   static constexpr uint32_t OFF = group_offset(G);
-  static constexpr uint32_t INV32 = inv32_mod(group_period(G));
 };
 
 // OR the table words of groups G..NG-1 for the current segment word and
-// advance their indices by nt words (compile-time recursion: constant moduli).
+// advance their indices (compile-time recursion: constant moduli).
 template <int G, int NG>
 __device__ __forceinline__ uint32_t wheel_word(const uint32_t *tab, uint32_t (&ig)[NG],
                                                const uint32_t (&dg)[NG]) {
@@ -110,17 +133,14 @@ __device__ __forceinline__ uint32_t wheel_word(const uint32_t *tab, uint32_t (&i
   }
 }
 
-// word index of segment word `tid`: (base * 32^-1 + tid) mod P, base = the
-// pattern bit of the segment's first slot
 template <int G, int NG>
-__device__ __forceinline__ void wheel_setup(uint32_t (&ig)[NG], uint32_t (&dg)[NG], uint64_t base,
+__device__ __forceinline__ void wheel_setup(uint32_t (&ig)[NG], uint32_t (&dg)[NG], uint64_t X0,
                                             uint32_t tid, uint32_t nt) {
   if constexpr (G < NG) {
     constexpr uint32_t P = WheelGroup<G>::P;
-    const uint32_t c0 = (uint32_t)((base % P) * WheelGroup<G>::INV32 % P);
-    ig[G] = (c0 + tid % P) % P;
-    dg[G] = nt % P;
-    wheel_setup<G + 1, NG>(ig, dg, base, tid, nt);
+    ig[G] = (uint32_t)((X0 % P + 1024u * (tid >> 5) + (tid & 31u)) % P);
+    dg[G] = (32u * nt) % P;
+    wheel_setup<G + 1, NG>(ig, dg, X0, tid, nt);
   }
 }
 
@@ -128,29 +148,27 @@ template <int NG>
 __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, uint64_t o0,
                                            uint64_t bit0, uint32_t valid, uint64_t a) {
   const uint32_t nt = blockDim.x, tid = threadIdx.x;
-  const uint32_t nwords = ((valid + 127u) >> 7) << 2;
-  // table index of word w: ((o0-1)/2 + bit0 + 32*w) mod P_g
+  const uint32_t nwords = ((valid + 1023u) >> 10) << 5;
   uint32_t ig[NG], dg[NG];
   wheel_setup<0, NG>(ig, dg, ((o0 - 1) >> 1) + bit0, tid, nt);
-  // fast path: words with no fix-up (first integer > w) and no tail slot
-  const uint64_t nfix = a > wheel_bound(NG) ? 0ull : (wheel_bound(NG) - a) / 64 + 1;
-  const uint32_t wfast_lo = nfix < nwords ? (uint32_t)nfix : nwords;
-  const uint32_t wfast_hi = valid >> 5;  // words [.., valid/32) are entirely valid
+  // fast path: words of whole blocks with no fix-up (block 0 holds the
+  // integers <= w when a <= w) and no tail slot
+  const uint32_t wfast_lo = a <= wheel_bound(NG) ? 32u : 0u;
+  const uint32_t wfast_hi = (valid >> 10) << 5;
   uint32_t w = tid;
   if (wfast_lo == 0) {
     for (; w < wfast_hi; w += nt) seg[w] = wheel_word<0, NG>(tab, ig, dg);
   }
   for (; w < nwords; w += nt) {
     uint32_t v = wheel_word<0, NG>(tab, ig, dg);
-    const uint64_t n0 = a + 64ull * w;  // odd integer of the word's bit 0
-    if (n0 <= wheel_bound(NG)) {
-      for (uint32_t b = 0; b < 32u && n0 + 2ull * b <= wheel_bound(NG); ++b) {
-        const uint32_t n = (uint32_t)(n0 + 2ull * b);
-        if (n == 1u) v |= 1u << b;  // 1 is not prime (reading R2)
-        else if ((kOddPrimesBelow64 >> n) & 1ull) v &= ~(1u << b);
-      }
+    const uint32_t b = w & 31u, j0 = ((w >> 5) << 10) + b;  // slot of the word's bit 0
+    if (w < 32u) {  // bit 0 <-> n = a + 2b (a <= w: n <= 2w+63, bits >= 1 are > w)
+      const uint64_t n = a + 2ull * b;
+      if (n == 1u) v |= 1u;  // 1 is not prime (reading R2)
+      else if (n < 64 && ((kOddPrimesBelow64 >> n) & 1ull) && n <= wheel_bound(NG)) v &= ~1u;
     }
-    const int k = (int)valid - (int)(w << 5);  // valid slots in this word
+    // valid bits i: j0 + 32 i < valid
+    const int k = j0 < valid ? (int)((valid - j0 + 31u) >> 5) : 0;
     if (k < 32) v = k <= 0 ? 0xFFFFFFFFu : (v | (0xFFFFFFFFu << k));
     seg[w] = v;
   }
@@ -158,98 +176,102 @@ __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, u
 
 struct PrimeRegions {
   uint32_t start;  // first marking prime (after the wheel primes)
-  uint32_t mid;    // first prime with fewer than kSmallHits hits per full segment
-  uint32_t skew;   // first prime with fewer than kSkewHits hits per full segment
-  uint32_t lanes;  // first prime with fewer than kLaneHits hits per full segment
+  uint32_t unit;   // first prime with fewer than kUnitHits hits per full segment
+  uint32_t cls;    // first prime with fewer than kClassHits hits per full segment
+  uint32_t warp;   // first prime with fewer than kWarpHits hits per full segment
   uint32_t end;    // first prime > r
 };
 
 // Mark bit `mask` of the words at byte offsets A, A+step, ... < alim of the
-// segment: the hits of one lane that share a bit position (2-3 instructions
-// per mark: the address add and the atomic, plus a guard per 4 marks).
-__device__ __forceinline__ void mark_run(char *segb, uint32_t A, uint32_t alim, uint32_t step,
-                                         uint32_t mask) {
+// segment: the hits of one residue class mod 1024 (2 instructions per mark:
+// the address add and the atomic, plus a guard per 4 marks).
+__device__ __forceinline__ void mark_run(uint32_t A, uint32_t alim, uint32_t step, uint32_t mask) {
   for (; A + 3u * step < alim; A += 4u * step) {
-    atomicOr(reinterpret_cast<uint32_t *>(segb + A), mask);
-    atomicOr(reinterpret_cast<uint32_t *>(segb + A + step), mask);
-    atomicOr(reinterpret_cast<uint32_t *>(segb + A + 2u * step), mask);
-    atomicOr(reinterpret_cast<uint32_t *>(segb + A + 3u * step), mask);
+    red_or(A, mask);
+    red_or(A + step, mask);
+    red_or(A + 2u * step, mask);
+    red_or(A + 3u * step, mask);
   }
   if (A < alim) {
-    atomicOr(reinterpret_cast<uint32_t *>(segb + A), mask);
+    red_or(A, mask);
     if (A + step < alim) {
-      atomicOr(reinterpret_cast<uint32_t *>(segb + A + step), mask);
-      if (A + 2u * step < alim) atomicOr(reinterpret_cast<uint32_t *>(segb + A + 2u * step), mask);
+      red_or(A + step, mask);
+      if (A + 2u * step < alim) red_or(A + 2u * step, mask);
     }
   }
 }
 
+// Byte limit of the residue class mod 1024 through slot j (bank b = j & 31):
+// its slots are j + 1024 p s at bytes 4 b + 128 (block), and slot < valid
+// <=> block < VB + [(j & 1023) < (valid & 1023)], VB = valid >> 10.
+__device__ __forceinline__ uint32_t class_limit(uint32_t j, uint32_t valid) {
+  const uint32_t lim = (valid >> 10) + ((j & 1023u) < (valid & 1023u) ? 1u : 0u);
+  return ((j & 31u) << 2) + (lim << 7);
+}
+
 // A4/A5: mark the odd multiples of every base prime in [R.start, R.end).
-//
-// Hit k of prime p in the segment is slot j0 + k p.  Hits k and k + 32 have
-// the same bit (32 p bits = p whole words apart), so a lane that walks every
-// 32nd hit -- one residue class mod 32 -- keeps one mask and adds 4p to a byte
-// address per atomic.  Regions by hits per segment K ~ S/p (DESIGN.md
-// "Marking"):
-//  (i)  K >= kSkewHits: work units of kPieceHits consecutive hits of one
-//       prime, round robin over warps.  Lane l owns residue class l of the
-//       unit; its word at class step m is W_l + p m.  The lane starts its
-//       class at the rotation sigma_l = (l - W_l) p^-1 (mod 32) and walks it
-//       in rounds of 32 steps (mod 32), so at step t its bank is l + p t
-//       (mod 32): the 32 lanes of every atomic hit 32 distinct banks.
-//  (ii) 64 <= K < kSkewHits: one prime per warp, lane l takes hits l + 32 s.
-//  (iii) K < kLaneHits: one prime per lane, unrolled by 4.
-// Region (ii) computes first hits 32 primes at a time (one Barrett reduction
-// per lane) and broadcasts them with shuffles.
-__device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__restrict__ primes,
+// Hit k of prime p in the segment is slot j0 + k p.  In the transposed
+// layout the bank of slot j is j mod 32, so (p odd):
+//  * 32 consecutive hits of p sit in 32 distinct banks;
+//  * hits k and k + 1024 (one residue class mod 1024) share bank and bit
+//    position and sit 32 p words apart: a lane walking a class keeps one mask
+//    and adds 128 p bytes per atomic, and 32 consecutive classes are 32 banks.
+// Regions by K = S/p (internal.h):
+//  (A1) K >= kUnitHits: units (prime, group g of 32 classes) round robin over
+//       the warps; lane l walks class 32 g + l.
+//  (A2) kClassHits <= K < kUnitHits: one prime per warp; lane l walks the
+//       classes l, l + 32, ..., l + 992 (moving from one class to the next is
+//       a rotation of the mask and an add: slot + 32 p).
+//  (B)  kWarpHits <= K < kClassHits: one prime per warp; lane l takes the
+//       hits l + 32 s (row += p, mask rotated by p per hit).
+//  (C)  K < kWarpHits: one prime per lane, unrolled by kLargeILP loads.
+// Every atomic of (A1)-(B) is conflict-free; (C) has random banks.  First
+// hits come from a Barrett reduction, 32 primes per warp at a time, with
+// shuffle broadcast; p^2 >= segment end stops a warp.  Work is dealt
+// statically: (A2) and (B) prime i to warp i mod nw, (C) prime i to thread
+// i mod nt, so every warp gets the same mix of small and large primes.
+__device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__restrict__ primes,
                                              const uint64_t *__restrict__ recips,
                                              const PrimeRegions R,
                                              uint64_t a, uint32_t valid, unsigned long long *prof) {
   const long long t0 = prof ? clock64() : 0;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t seg_end = a + 2ull * valid;
-  char *segb = reinterpret_cast<char *>(seg);
-  const uint32_t vw = valid >> 5, vb = valid & 31u;
+  const bool whole = (valid & 1023u) == 0;  // every class has the same block limit
 
-  // (i) small primes
+  // (A1) units (prime, class group), dealt round robin over the warps:
+  // unit 32 i + g goes to warp (32 i + g) mod nw, rot = 32 i mod nw
   const uint32_t c32 = 32u % nw;
   uint32_t rot = (32u * R.start) % nw;
-  for (uint32_t ib = R.start; ib < R.mid; ib += 32) {
+  for (uint32_t ib = R.start; ib < R.unit; ib += 32) {
     const uint32_t i = ib + lane;
     uint32_t pl = 0, jl = kNone;
-    if (i < R.mid) {
+    if (i < R.unit) {
       pl = __ldg(primes + i);
       jl = first_hit(a, seg_end, pl, __ldg(recips + i));
     }
-    const uint32_t nb = min(32u, R.mid - ib);
+    const uint32_t nb = min(32u, R.unit - ib);
     for (uint32_t k = 0; k < nb; ++k) {
       const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
       const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
       if (j0 == kNone) break;  // p^2 past the segment, and so for every later prime
-      // (prime, residue) units are dealt round robin over the warps:
-      // unit 32 i + r goes to warp (32 i + r) mod nw, rot = 32 i mod nw
-      const uint32_t r0 = warp >= rot ? warp - rot : warp + nw - rot;
+      const uint32_t g0 = warp >= rot ? warp - rot : warp + nw - rot;
       rot += c32;
       if (rot >= nw) rot -= nw;
-      for (uint32_t r = r0; r < 32u; r += nw) {
-        const uint32_t jr = j0 + r * p;  // first hit of residue class r
-        if (jr >= valid) break;
-        const uint32_t bit = jr & 31u;
-        mark_run(segb, ((jr >> 5) + lane * p) << 2, (vw + (bit < vb ? 1u : 0u)) << 2, 128u * p,
-                 1u << bit);
+      for (uint32_t g = g0; g < 32u; g += nw) {
+        const uint32_t j = j0 + (32u * g + lane) * p;  // first hit of class 32 g + lane
+        mark_run(sb + t_addr(j), sb + class_limit(j, valid), 128u * p, t_mask(j));
       }
     }
   }
   const long long t1 = prof ? clock64() : 0;
-  // (ii-a) medium primes with >= kSkewHits hits: one prime per warp, lane l
-  // owns residue class l (hits l + 32m, one bit, words W_l + p m).  The lane
-  // starts its class at a rotation sigma_l chosen so that its bank at step t
-  // is l + p t (mod 32): all 32 lanes of every atomic in distinct banks.
-  // Rotation is mod 32 hits, which shifts a word by 32 p == 0 (mod 32) banks.
-  for (uint32_t ib = R.mid + warp; ib < R.skew; ib += 32u * nw) {
+
+  // (A2) one prime per warp, lane l walks the classes l + 32 g
+  // (few primes, each a lot of work: static, warp w takes primes w + nw l)
+  for (uint32_t ib = R.unit + warp; ib < R.cls; ib += 32u * nw) {
     const uint32_t i = ib + lane * nw;
     uint32_t pl = 0, jl = kNone;
-    if (i < R.skew) {
+    if (i < R.cls) {
       pl = __ldg(primes + i);
       jl = first_hit(a, seg_end, pl, __ldg(recips + i));
     }
@@ -257,68 +279,81 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
     for (uint32_t k = 0; k < 32u; ++k) {
       const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
       const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
-      if (j0 == kNone) { stop = true; break; }
-      const uint32_t j = j0 + lane * p;          // first hit of class `lane`
-      const uint32_t bit = j & 31u, mask = 1u << bit;
-      const uint32_t w = j >> 5;
-      const uint32_t alim = (vw + (bit < vb ? 1u : 0u)) << 2;
-      const uint32_t step = 4u * p, span = 128u * p;
-      const uint32_t pinv = p * (2u - p * p);     // p^-1 mod 32 (Newton step from p^-1 = p mod 8)
-      uint32_t B = w << 2;
-      const uint32_t nh = B < alim ? (alim - B + step - 1u) / step : 0u;  // hits of this class
-      const uint32_t full = nh >> 5;  // lanes differ by at most one chunk
-      if (full) {
-        // the 32 rotated byte offsets of a round, computed once per prime
-        uint32_t off[32];
-        off[0] = (((lane - w) * pinv) & 31u) * step;
-#pragma unroll
-        for (int t = 1; t < 32; ++t) {
-          const uint32_t x = off[t - 1] + step;
-          off[t] = min(x, x - span);
-        }
-        char *base = segb + B;
-        for (uint32_t c = 0; c < full; ++c, base += span) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) atomicOr(reinterpret_cast<uint32_t *>(base + off[t]), mask);
-        }
-        B += full * span;
-      }
-      mark_run(segb, B, alim, step, mask);  // the last < 32 hits in plain order
-    }
-    if (stop) break;
-  }
-  const long long t1b = prof ? clock64() : 0;
-  (void)t1b;
-  // (ii-b) medium primes: prime i = R.skew + warp + nw*t, batches of 32 t's
-  for (uint32_t ib = R.skew + warp; ib < R.lanes; ib += 32u * nw) {
-    const uint32_t i = ib + lane * nw;
-    uint32_t pl = 0, jl = kNone;
-    if (i < R.lanes) {
-      pl = __ldg(primes + i);
-      jl = first_hit(a, seg_end, pl, __ldg(recips + i));
-    }
-    bool stop = false;
-    for (uint32_t k = 0; k < 32u; ++k) {
-      const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
-      const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
-      if (j0 == kNone) { stop = true; break; }
-      const uint32_t j = j0 + lane * p;  // this lane's first hit
-      if (j < valid) {
-        const uint32_t bit = j & 31u;
-        mark_run(segb, (j >> 5) << 2, (vw + (bit < vb ? 1u : 0u)) << 2, 4u * p, 1u << bit);
+      if (j0 == kNone) { stop = true; break; }  // and so for every later prime
+      uint32_t j = j0 + lane * p;  // first hit of class `lane`
+      uint32_t mask = t_mask(j);
+      const uint32_t step = 128u * p, dj = 32u * p;
+      if (whole) {
+        const uint32_t alim = sb + ((j & 31u) << 2) + ((valid >> 10) << 7);
+        for (uint32_t g = 0; g < 32u; ++g, j += dj, mask = rotl(mask, p))
+          mark_run(sb + t_addr(j), alim, step, mask);
+      } else {
+        for (uint32_t g = 0; g < 32u; ++g, j += dj, mask = rotl(mask, p))
+          mark_run(sb + t_addr(j), sb + class_limit(j, valid), step, mask);
       }
     }
     if (stop) break;
   }
   const long long t2 = prof ? clock64() : 0;
-  // (iii) large primes: lane per prime (few hits each).  Each thread takes
-  // kLargeILP primes per iteration and issues all their loads and Barrett
-  // reductions before marking, so the L2 latency of the prime list overlaps.
-  for (uint32_t k0 = R.lanes + threadIdx.x; k0 < R.end; k0 += kLargeILP * blockDim.x) {
+
+  // (B) one prime per warp, lane l takes the hits l + 32 s: slot j advances
+  // by 32 p, i.e. its row j >> 5 by p (bank fixed), so the byte offset is
+  // (4 row) & ~127 | 4 bank and the mask rotates by p.
+  for (uint32_t ib = R.cls + warp; ib < R.warp; ib += 32u * nw) {
+    const uint32_t i = ib + lane * nw;
+    uint32_t pl = 0, jl = kNone;
+    if (i < R.warp) {
+      pl = __ldg(primes + i);
+      jl = first_hit(a, seg_end, pl, __ldg(recips + i));
+    }
+    bool stop = false;
+    for (uint32_t k = 0; k < 32u; ++k) {
+      const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
+      const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
+      if (j0 == kNone) { stop = true; break; }  // and so for every later prime
+      const uint32_t j = j0 + lane * p;
+      const uint32_t b4 = (j & 31u) << 2;
+      // Q = shared byte address of the hit's block plus 4 (row & 31): the
+      // 128-byte aligned base keeps (Q & ~127) | b4 the hit's word
+      uint32_t Q = sb + ((j >> 5) << 2);
+      uint32_t mask = t_mask(j);
+      // slot < valid <=> row < ceil((valid - bank) / 32) (0 when bank >= valid)
+      const uint32_t Qlim = sb + (((valid + 31u - (j & 31u)) >> 5) << 2);
+      const uint32_t s4 = 4u * p;
+      for (; Q + 3u * s4 < Qlim; Q += 4u * s4) {
+        red_or((Q & ~127u) | b4, mask);
+        mask = rotl(mask, p);
+        red_or(((Q + s4) & ~127u) | b4, mask);
+        mask = rotl(mask, p);
+        red_or(((Q + 2u * s4) & ~127u) | b4, mask);
+        mask = rotl(mask, p);
+        red_or(((Q + 3u * s4) & ~127u) | b4, mask);
+        mask = rotl(mask, p);
+      }
+      if (Q < Qlim) {  // the last < 4 hits, predicated
+        red_or((Q & ~127u) | b4, mask);
+        if (Q + s4 < Qlim) {
+          red_or(((Q + s4) & ~127u) | b4, rotl(mask, p));
+          if (Q + 2u * s4 < Qlim) red_or(((Q + 2u * s4) & ~127u) | b4, rotl(mask, 2u * p));
+        }
+      }
+    }
+    if (stop) break;
+  }
+  const long long t3 = prof ? clock64() : 0;
+
+  // (C) large primes: lane per prime (few hits each).  Thread t takes the
+  // primes t + nt m, kLargeILP at a time, and issues all their loads and
+  // Barrett reductions before marking, so the L2 latency of the prime list
+  // overlaps.  The lane walks J = 4 j + 32 sb: the byte offset
+  // of slot j is (J >> 5) & ~127 | J & 127 and its bit is (J >> 7) & 31 (the
+  // base term is a multiple of 4096, invisible to both).
+  const uint32_t Jlim = 4u * valid + 32u * sb;
+  for (uint32_t k0 = R.warp + threadIdx.x; k0 < R.end; k0 += kLargeILP * blockDim.x) {
     uint32_t pk[kLargeILP], jk[kLargeILP];
     uint64_t rk[kLargeILP];
 #pragma unroll
-    for (int u = 0; u < kLargeILP; ++u) {  // all loads first (clamped index: no branch)
+    for (int u = 0; u < kLargeILP; ++u) {
       const uint32_t k = min(k0 + u * blockDim.x, R.end - 1u);
       pk[u] = __ldg(primes + k);
       rk[u] = __ldg(recips + k);
@@ -331,25 +366,46 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
     if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
 #pragma unroll
     for (int u = 0; u < kLargeILP; ++u) {
-      const uint32_t p = pk[u];
-      uint32_t j = jk[u];
-      if (j == kNone) break;
-      for (; j + 3u * p < valid; j += 4u * p) {
-        mark(seg, j);
-        mark(seg, j + p);
-        mark(seg, j + 2u * p);
-        mark(seg, j + 3u * p);
+      if (jk[u] == kNone) break;
+      const uint32_t P4 = 4u * pk[u];
+      uint32_t J = 4u * jk[u] + 32u * sb;
+      for (; J + 3u * P4 < Jlim; J += 4u * P4) {
+        red_or(j_addr(J), j_mask(J));
+        red_or(j_addr(J + P4), j_mask(J + P4));
+        red_or(j_addr(J + 2u * P4), j_mask(J + 2u * P4));
+        red_or(j_addr(J + 3u * P4), j_mask(J + 3u * P4));
       }
-      for (; j < valid; j += p) mark(seg, j);
+      for (; J < Jlim; J += P4) red_or(j_addr(J), j_mask(J));
     }
   }
-  if (prof) {  // per-warp busy cycles of the three regions (diagnostics only)
-    const long long t3 = clock64();
+  if (prof) {  // per-warp busy cycles of the regions (diagnostics only)
+    const long long t4 = clock64();
     if ((threadIdx.x & 31u) == 0) {
       atomicAdd(prof + 3, (unsigned long long)(t1 - t0));
       atomicAdd(prof + 4, (unsigned long long)(t2 - t1));
       atomicAdd(prof + 5, (unsigned long long)(t3 - t2));
+      atomicAdd(prof + 7, (unsigned long long)(t4 - t3));
     }
+  }
+}
+
+// In-place 32x32 bit transpose of every 1024-slot block of the segment
+// (transposed layout -> natural layout: word w holds slots 32 w .. 32 w + 31,
+// LSB first), one block per warp at a time.  Lane r holds row r; stage w
+// swaps the off-diagonal w x w sub-blocks of every 2w x 2w block.
+__device__ __forceinline__ void untranspose(uint32_t *seg, uint32_t valid) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t nblk = (valid + 1023u) >> 10;
+  for (uint32_t B = warp; B < nblk; B += nw) {
+    uint32_t x = seg[32u * B + lane];
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+      const uint32_t m = w == 16 ? 0x0000FFFFu : w == 8 ? 0x00FF00FFu : w == 4 ? 0x0F0F0F0Fu
+                       : w == 2 ? 0x33333333u : 0x55555555u;  // columns c with (c & w) == 0
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, x, w);
+      x = (lane & w) ? ((x & ~m) | ((y >> w) & m)) : ((x & m) | ((y << w) & ~m));
+    }
+    seg[32u * B + lane] = x;
   }
 }
 
@@ -357,11 +413,16 @@ __device__ __forceinline__ void mark_segment(uint32_t *seg, const uint32_t *__re
 //
 // Sum of the primes of the segment = C*a + 2*J, where a is the segment's
 // first odd integer, C the number of set (prime) bits and J the sum of their
-// bit positions j = 128 q + 32 x + b (quad q, word x, bit b).  Per quad the
-// thread needs the quad's popcount (for C and 128 q c_q) and the word
-// popcounts (for 32 x); the bit-position part sum_b b * n_b is accumulated
-// without popcounts in carry-save bit planes (Harley-Seal adder tree: plane
-// k holds bit k of the per-position count n_b), and read once per segment.
+// slots j.  Per quad the thread needs the quad's popcount (for C and the
+// quad's weight) and the word popcounts; the bit-position part sum_b b * n_b
+// is accumulated without popcounts in carry-save bit planes (Harley-Seal
+// adder tree: plane k holds bit k of the per-position count n_b), and read
+// once per segment.
+//  * natural layout (bitmap mode, after untranspose): word 4q + e, bit b is
+//    slot 128 q + 32 e + b;
+//  * transposed layout (count and batch modes): word 4q + e, bit i is slot
+//    1024 (q >> 3) + 4 (q & 7) + e + 32 i = 128 q - 124 (q & 7) + e + 32 i,
+//    and q & 7 = tid & 7 for every quad of a thread (nt is a multiple of 8).
 __device__ __forceinline__ void csa(uint32_t &carry, uint32_t &sum, uint32_t a, uint32_t b,
                                     uint32_t c) {
   const uint32_t u = a ^ b;
@@ -374,12 +435,13 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
                                          uint32_t valid, uint32_t *out, uint64_t out_words,
                                          uint32_t vec4, unsigned long long &cnt,
                                          unsigned long long &sum) {
-  const uint32_t nq = (valid + 127u) >> 7;
+  constexpr bool kNatural = MODE == kBitmap;
+  const uint32_t nq = kNatural ? (valid + 127u) >> 7 : ((valid + 1023u) >> 10) << 3;
   const uint4 *seg4 = reinterpret_cast<const uint4 *>(seg);
   const uint64_t w0 = bit0 >> 5;  // first word of the segment in the call's grid
-  // planes of per-bit-position counts (counts < 256 for <= 63 quads per thread)
+  // planes of per-bit-position counts (counts < 512: <= 127 quads per thread)
   uint32_t ones = 0, twos = 0, fours = 0, p8 = 0, p16 = 0, p32 = 0, p64 = 0, p128 = 0;
-  uint32_t C = 0, X = 0, Q = 0;  // count, sum of 32x over set bits / 32, sum of k c_k
+  uint32_t C = 0, X = 0, Q = 0;  // count, sum of e c_e, sum of k c_k
   uint32_t k = 0;
   for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x, ++k) {
     const uint4 v = seg4[q];
@@ -412,13 +474,14 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
       }
     }
   }
-  // sum of bit positions b over all set bits = sum_k 2^k bit_index_sum(plane_k)
-  const uint32_t B = bit_index_sum(ones) + 2u * bit_index_sum(twos) + 4u * bit_index_sum(fours) +
-                     8u * bit_index_sum(p8) + 16u * bit_index_sum(p16) + 32u * bit_index_sum(p32) +
-                     64u * bit_index_sum(p64) + 128u * bit_index_sum(p128);
+  // sum of bit positions over all set bits = sum_k 2^k bit_index_sum(plane_k)
+  const uint32_t Bs = bit_index_sum(ones) + 2u * bit_index_sum(twos) + 4u * bit_index_sum(fours) +
+                      8u * bit_index_sum(p8) + 16u * bit_index_sum(p16) + 32u * bit_index_sum(p32) +
+                      64u * bit_index_sum(p64) + 128u * bit_index_sum(p128);
   // sum of 128 q over set bits, q = tid + k nt
   const uint64_t Jq = 128ull * ((uint64_t)threadIdx.x * C + (uint64_t)blockDim.x * Q);
-  const uint64_t J = Jq + 32ull * X + B;
+  const uint64_t J = kNatural ? Jq + 32ull * X + Bs
+                              : Jq - 124ull * (threadIdx.x & 7u) * C + X + 32ull * Bs;
   cnt += C;
   sum += (unsigned long long)C * a + 2ull * J;
 }
@@ -471,8 +534,8 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
   const uint32_t nb = *P.nbase;
   if (warp < (only_end ? 1u : 4u)) {
     const uint64_t x = warp == 0 ? (uint64_t)r
-                     : warp == 1 ? P.seg_bits / kSmallHits
-                     : warp == 2 ? P.seg_bits / kSkewHits : P.seg_bits / kLaneHits;
+                     : warp == 1 ? P.seg_bits / kUnitHits
+                     : warp == 2 ? P.seg_bits / kClassHits : P.seg_bits / kWarpHits;
     const uint32_t u = warp_upper_bound(P.primes, nb, x);
     if ((threadIdx.x & 31u) == 0) scratch[warp] = u;
   }
@@ -480,9 +543,9 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
   if (threadIdx.x == 0) {
     R.end = scratch[0];
     R.start = min(ng_start, R.end);
-    R.mid = max(R.start, min(R.end, scratch[1]));
-    R.skew = max(R.mid, min(R.end, scratch[2]));
-    R.lanes = max(R.skew, min(R.end, scratch[3]));
+    R.unit = max(R.start, min(R.end, scratch[1]));
+    R.cls = max(R.unit, min(R.end, scratch[2]));
+    R.warp = max(R.cls, min(R.end, scratch[3]));
   }
 }
 
@@ -495,8 +558,12 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
 template <int NG, int MODE>
 __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
-  uint32_t *seg = smem;
-  uint32_t *tab = smem + P.seg_bits / 32;
+  // segment at the first 128-byte boundary of the dynamic shared memory (the
+  // runtime allocates kSmemAlign spare bytes), wheel tables after it
+  const uint32_t sraw = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t sb = (sraw + (kSmemAlign - 1u)) & ~(kSmemAlign - 1u);
+  uint32_t *seg = smem + (sb - sraw) / 4u;
+  uint32_t *tab = seg + P.seg_bits / 32;
   __shared__ unsigned long long red[64];
   __shared__ PrimeRegions sR;
   __shared__ uint32_t s_last;
@@ -525,7 +592,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     wheel_init<NG>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
-    if (!(P.flags & kFlagSkipMarking)) mark_segment(seg, P.primes, P.recips, sR, a, valid, P.prof);
+    if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, sR, a, valid, P.prof);
     __syncthreads();
     const long long c2 = P.prof ? clock64() : 0;
     if (MODE == kBatch) {
@@ -539,6 +606,8 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       }
       __syncthreads();
     } else if (MODE == kBitmap && P.seg_counts) {
+      untranspose(seg, valid);
+      __syncthreads();
       unsigned long long c = 0, sm = 0;
       epilogue<kBitmap>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, c, sm);
       cnt += c;
@@ -548,6 +617,10 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       if (threadIdx.x == 0) P.seg_counts[s] = (uint32_t)c2;
       __syncthreads();
     } else {
+      if (MODE == kBitmap) {
+        untranspose(seg, valid);
+        __syncthreads();
+      }
       epilogue<MODE>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
       __syncthreads();
     }

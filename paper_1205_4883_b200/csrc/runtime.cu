@@ -153,8 +153,8 @@ int ng_for_wheel(uint32_t w) {
   }
 }
 
-// word table g: WT[k] bit b = 1 iff 2i+1 is divisible by a prime of group g,
-// i = (32k + b) mod P_g
+// transposed word table g (internal.h): TT[y] bit i = 1 iff 2x+1 is divisible
+// by a prime of group g, x = (y + 32 i) mod P_g
 void build_tables(std::vector<uint32_t> &t) {
   static const uint32_t groups[sv::kMaxGroups][4] = {
       {3, 5, 7, 11}, {13, 17, 0, 0}, {19, 23, 0, 0}, {29, 31, 0, 0}, {37, 41, 0, 0}, {43, 47, 0, 0}};
@@ -162,13 +162,13 @@ void build_tables(std::vector<uint32_t> &t) {
   for (int g = 0; g < sv::kMaxGroups; ++g) {
     const uint32_t P = sv::group_period(g);
     uint32_t *w = t.data() + sv::group_offset(g);
-    for (uint32_t k = 0; k < P; ++k)
-      for (uint32_t b = 0; b < 32; ++b) {
-        const uint64_t i = (32ull * k + b) % P;
-        const uint64_t n = 2 * i + 1;
+    for (uint32_t y = 0; y < P; ++y)
+      for (uint32_t i = 0; i < 32; ++i) {
+        const uint64_t x = (y + 32ull * i) % P;
+        const uint64_t n = 2 * x + 1;
         bool hit = false;
         for (int q = 0; q < 4 && groups[g][q]; ++q) hit |= (n % groups[g][q]) == 0;
-        if (hit) w[k] |= 1u << b;
+        if (hit) w[y] |= 1u << i;
       }
   }
 }
@@ -198,7 +198,7 @@ int ensure_ready() {
 
 size_t seg_bits() { return (size_t)g.opt.segment_kb * 8192; }
 size_t smem_for(uint32_t segment_kb, uint32_t wheel) {
-  return (size_t)segment_kb * 1024 + sv::tables_words(ng_for_wheel(wheel)) * 4;
+  return (size_t)segment_kb * 1024 + sv::tables_words(ng_for_wheel(wheel)) * 4 + sv::kSmemAlign;
 }
 size_t sieve_smem() { return smem_for(g.opt.segment_kb, g.opt.wheel); }
 

@@ -119,7 +119,7 @@ def test_bitmap_multi_segment_ragged(seg_kb, wheel):
         assert sv.stats(lo, hi) == (oc, os_)
 
 
-@pytest.mark.parametrize("threads", [256, 512, 768])
+@pytest.mark.parametrize("threads", [256, 512, 768, 1024])
 def test_thread_and_occupancy_invariance(threads):
     sv.set_options(threads=threads, segment_kb=64, ctas_per_sm=2)
     lo, hi = 10**11, 10**11 + 5 * 10**7 + 3

@@ -1,33 +1,34 @@
-"""Summarise an ncu source page (cuda,sass view) per CUDA source line:
-warp-stall samples, executed warp instructions and shared wavefronts."""
-import csv, subprocess, sys
+"""Per-source-line summary of an ncu report (cuda,sass source view): warp-stall
+samples, instructions executed and shared-memory wavefronts (actual / ideal)
+for the hottest lines.  Usage: python tools/ncu_lines.py REPORT [N]"""
+import csv
+import io
+import subprocess
+import sys
+
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
-rows = list(csv.reader(out.splitlines()))
-hdr, fname, res = None, "", []
+rows = list(csv.reader(io.StringIO(out)))
+hdr = None
+lines = []
 for r in rows:
-    if len(r) == 2 and r[0] == "File Path":
-        fname = r[1].split("/")[-1]
-        continue
     if r and r[0] == "Line No":
         hdr = r
         continue
-    if not hdr or len(r) != len(hdr) or not r[0]:
-        continue
-    def g(k):
-        i = hdr.index(k)
-        try:
-            return int(r[i])
-        except ValueError:
-            return 0
-    s, ie = g("Warp Stall Sampling (All Samples)"), g("Instructions Executed")
-    if s or ie:
-        res.append((s, ie, fname, r[0], r[1].strip()[:80], g("L1 Wavefronts Shared"),
-                    g("L1 Wavefronts Shared Ideal")))
-tot = sum(x[0] for x in res) or 1
-toti = sum(x[1] for x in res) or 1
-print(f"total samples {tot}, warp instructions {toti}")
-for s, ie, f, ln, src, wf, wfi in sorted(res, reverse=True)[:n]:
-    print(f"{100*s/tot:5.1f}% {100*ie/toti:5.1f}%i {f}:{ln:>4} wf={wf}/{wfi} {src}")
+    if hdr and r and r[0].isdigit():
+        d = dict(zip(hdr[2:], r[2:]))  # metric columns follow "Line No","Source"
+        def g(k):
+            try:
+                return float(d.get(k, "0") or 0)
+            except ValueError:
+                return 0.0
+        lines.append((int(r[0]), r[1][:70], g("Warp Stall Sampling (All Samples)"),
+                      g("Instructions Executed"), g("L1 Wavefronts Shared"), g("L1 Wavefronts Shared Ideal")))
+tot_s = sum(x[2] for x in lines) or 1
+tot_i = sum(x[3] for x in lines) or 1
+print(f"total samples {tot_s:.0f}  instructions {tot_i:.3e}  smem wavefronts {sum(x[4] for x in lines):.3e}"
+      f" (ideal {sum(x[5] for x in lines):.3e})")
+for ln, src, s, i, wf, wi in sorted(lines, key=lambda x: -x[2])[:n]:
+    print(f"{ln:5d} samp {100*s/tot_s:5.1f}%  inst {100*i/tot_i:5.1f}%  wf {wf:11.0f} ideal {wi:11.0f}  {src}")

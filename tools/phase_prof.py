@@ -22,5 +22,5 @@ for spec in sys.argv[1:] or [""]:
     print(json.dumps({"opts": o, "ms_with_prof": ev0.elapsed_time(ev1), "result": r,
           "segments": v[6], "cta_cycles_per_seg": cta / v[6],
           "init%": 100 * v[0] / cta, "mark%": 100 * v[1] / cta, "epi%": 100 * v[2] / cta,
-          "warp_small_per_seg": v[3] / v[6] / nw, "warp_medium_per_seg": v[4] / v[6] / nw,
-          "warp_large_per_seg": v[5] / v[6] / nw, "mark_cta_per_seg": v[1] / v[6]}))
+          "warp_A1_per_seg": v[3] / v[6] / nw, "warp_A2_per_seg": v[4] / v[6] / nw,
+          "warp_B_per_seg": v[5] / v[6] / nw, "warp_C_per_seg": v[7] / v[6] / nw, "mark_cta_per_seg": v[1] / v[6]}))
