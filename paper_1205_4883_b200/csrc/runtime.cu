@@ -595,8 +595,8 @@ int sieve_set_options(const sieve_options *o) {
     for (int i = 0; i < 4; ++i)
       if (o->reserved[i]) return fail(SIEVE_EINVAL, "reserved option fields must be zero");
     if (o->segment_kb) {
-      if (o->segment_kb % 16 != 0 || o->segment_kb > 208)
-        return fail(SIEVE_EINVAL, "segment_kb %u is not a multiple of 16 in [16, 208]", o->segment_kb);
+      if (o->segment_kb < 4 || o->segment_kb > 224)
+        return fail(SIEVE_EINVAL, "segment_kb %u is not in [4, 224]", o->segment_kb);
       n.segment_kb = o->segment_kb;
     }
     if (o->wheel) {

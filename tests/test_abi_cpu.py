@@ -44,7 +44,7 @@ def test_validation_before_device():
         sv.count(0, (1 << 48) + 1)
     assert e.value.code == -2
     with pytest.raises(sv.SieveError):
-        sv.set_options(segment_kb=40)
+        sv.set_options(segment_kb=3)
     with pytest.raises(sv.SieveError):
         sv.set_options(wheel=19)
     sv.set_options(segment_kb=64, wheel=47)
