@@ -61,7 +61,13 @@ typedef struct sieve_options {
                              segment + wheel tables must fit 226 KiB of shared memory */
     uint32_t ctas_per_sm; /* resident CTAs per SM for the sieve kernel (default: occupancy maximum) */
     uint32_t threads;     /* threads per CTA: a multiple of 64 in [256, 1024] (default 1024) */
-    uint32_t reserved[4]; /* must be zero */
+    uint32_t buckets;     /* step A5, primes p > S (at most one hit per segment of S odd slots):
+                             0 = one Barrett first-hit reduction per prime and segment (default:
+                             measured faster on B200 for every config);
+                             1 = per-segment buckets (a skipped segment costs the prime nothing;
+                             not used by sieve_batch, nor for ranges of more than 2^31 odd slots
+                             per CTA, where the Barrett path runs) */
+    uint32_t reserved[3]; /* must be zero */
 } sieve_options;
 
 /* ---------------------------------------------------------------------- */

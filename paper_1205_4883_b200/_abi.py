@@ -34,7 +34,7 @@ class SieveError(RuntimeError):
 class _Options(ctypes.Structure):
     _fields_ = [("segment_kb", ctypes.c_uint32), ("wheel", ctypes.c_uint32),
                 ("ctas_per_sm", ctypes.c_uint32), ("threads", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32 * 4)]
+                ("buckets", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 3)]
 
 
 _lib = None
@@ -187,8 +187,9 @@ def get_stream() -> int:
     return int(lib().sieve_get_stream() or 0)
 
 
-def set_options(segment_kb: int = 0, wheel: int = 0, ctas_per_sm: int = 0, threads: int = 0) -> None:
-    o = _Options(segment_kb, wheel, ctas_per_sm, threads)
+def set_options(segment_kb: int = 0, wheel: int = 0, ctas_per_sm: int = 0, threads: int = 0,
+                buckets: int = 0) -> None:
+    o = _Options(segment_kb, wheel, ctas_per_sm, threads, buckets)
     _check(lib().sieve_set_options(ctypes.byref(o)))
 
 
@@ -196,7 +197,7 @@ def get_options() -> dict:
     o = _Options()
     _check(lib().sieve_get_options(ctypes.byref(o)))
     return {"segment_kb": o.segment_kb, "wheel": o.wheel, "ctas_per_sm": o.ctas_per_sm,
-            "threads": o.threads}
+            "threads": o.threads, "buckets": o.buckets}
 
 
 def shutdown() -> None:

@@ -70,6 +70,20 @@ constexpr uint32_t kClassHits = SIEVE_CLASS_HITS;
 #define SIEVE_WARP_HITS 256
 #endif
 constexpr uint32_t kWarpHits = SIEVE_WARP_HITS;
+// step A5: primes with fewer than kBucketHits hits per full segment (p > S /
+// kBucketHits) go through per-segment buckets when enabled (option buckets)
+#ifndef SIEVE_BUCKET_HITS
+#define SIEVE_BUCKET_HITS 1
+#endif
+constexpr uint32_t kBucketHits = SIEVE_BUCKET_HITS;
+// ring of at most kMaxRing buckets per warp (a later hit is parked in the
+// last bucket and re-queued from there)
+constexpr uint32_t kMaxRing = 32;
+// bucket entries a lane loads at once when draining
+#ifndef SIEVE_DRAIN_ILP
+#define SIEVE_DRAIN_ILP 4
+#endif
+constexpr uint32_t kDrainILP = SIEVE_DRAIN_ILP;
 // primes a thread handles at once in the lane-per-prime region (load ILP)
 #ifndef SIEVE_LARGE_ILP
 #define SIEVE_LARGE_ILP 2
@@ -116,6 +130,14 @@ struct SieveParams {
   const BatchItem *items;  // batch mode
   unsigned long long *prof;  // optional phase-cycle counters (diagnostics), [8]
   uint32_t flags;            // diagnostics: kFlagSkipMarking
+  // step A5 buckets (nullptr: off).  CTA c sieves the contiguous segments
+  // [c nseg / grid, (c+1) nseg / grid); bucket (c, slot, warp) holds capw
+  // entries {p, slot offset relative to its segment} at
+  // buckets + ((c * ring + slot) * nwarps + warp) * capw.
+  uint2 *buckets;
+  uint32_t ring;     // ring size R (<= kMaxRing): a hit lands at most R-1 segments ahead
+  uint32_t capw;     // capacity of one bucket (>= bucket primes / warps, rounded up)
+  uint32_t inv_seg;  // ceil(2^32 / seg_bits): o / S by a multiply-high and one correction
 };
 
 // Diagnostic flag: skip step A4/A5 (wheel init + count/write-back only), to

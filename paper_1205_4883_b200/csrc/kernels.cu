@@ -179,6 +179,7 @@ struct PrimeRegions {
   uint32_t unit;   // first prime with fewer than kUnitHits hits per full segment
   uint32_t cls;    // first prime with fewer than kClassHits hits per full segment
   uint32_t warp;   // first prime with fewer than kWarpHits hits per full segment
+  uint32_t big;    // first bucket prime (fewer than kBucketHits hits; = end without buckets)
   uint32_t end;    // first prime > r
 };
 
@@ -224,7 +225,9 @@ __device__ __forceinline__ uint32_t class_limit(uint32_t j, uint32_t valid) {
 //       a rotation of the mask and an add: slot + 32 p).
 //  (B)  kWarpHits <= K < kClassHits: one prime per warp; lane l takes the
 //       hits l + 32 s (row += p, mask rotated by p per hit).
-//  (C)  K < kWarpHits: one prime per lane, unrolled by kLargeILP loads.
+//  (C)  K < kWarpHits: one prime per lane, unrolled by kLargeILP loads,
+//       except the bucket primes (K < kBucketHits, see bucket_drain) when the
+//       runtime enables buckets.
 // Every atomic of (A1)-(B) is conflict-free; (C) has random banks.  First
 // hits come from a Barrett reduction, 32 primes per warp at a time, with
 // shuffle broadcast; p^2 >= segment end stops a warp.  Work is dealt
@@ -349,19 +352,19 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // of slot j is (J >> 5) & ~127 | J & 127 and its bit is (J >> 7) & 31 (the
   // base term is a multiple of 4096, invisible to both).
   const uint32_t Jlim = 4u * valid + 32u * sb;
-  for (uint32_t k0 = R.warp + threadIdx.x; k0 < R.end; k0 += kLargeILP * blockDim.x) {
+  for (uint32_t k0 = R.warp + threadIdx.x; k0 < R.big; k0 += kLargeILP * blockDim.x) {
     uint32_t pk[kLargeILP], jk[kLargeILP];
     uint64_t rk[kLargeILP];
 #pragma unroll
     for (int u = 0; u < kLargeILP; ++u) {
-      const uint32_t k = min(k0 + u * blockDim.x, R.end - 1u);
+      const uint32_t k = min(k0 + u * blockDim.x, R.big - 1u);
       pk[u] = __ldg(primes + k);
       rk[u] = __ldg(recips + k);
     }
 #pragma unroll
     for (int u = 0; u < kLargeILP; ++u) {
       jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
-      if (k0 + u * blockDim.x >= R.end) jk[u] = kNone;
+      if (k0 + u * blockDim.x >= R.big) jk[u] = kNone;
     }
     if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
 #pragma unroll
@@ -387,6 +390,123 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
       atomicAdd(prof + 7, (unsigned long long)(t4 - t3));
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// A5: per-segment buckets for the large primes (K < kBucketHits), so that a
+// segment a prime does not hit costs it nothing.  A CTA sieves a contiguous
+// run of segments [s0, s1); warp w owns the bucket primes R.big + w + nw m.
+// An entry {p, o} in ring slot s mod R of warp w says: prime p next hits
+// slot o of segment s (o >= S: only parked there, re-queued further).  Per
+// segment the warp drains its slot: marks the hits o, o + p, ... < valid,
+// then re-queues p in the slot of its next segment s + d, 1 <= d < R.  The
+// fill counts of the warp's R slots live in registers (lane t: slot t); an
+// append ranks the lanes with the same target slot by one ballot per slot,
+// so there are no atomics on the bookkeeping and the entries are
+// warp-private.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint2 *bucket_at(const SieveParams &P, uint32_t slot, uint32_t warp,
+                                           uint32_t nw) {
+  return P.buckets + ((size_t)(blockIdx.x * P.ring + slot) * nw + warp) * P.capw;
+}
+
+// append e to ring slot `slot` for every lane with `alive`; cnt: lane t holds
+// the fill count of slot t
+__device__ __forceinline__ void bucket_push(const SieveParams &P, uint32_t &cnt, bool alive,
+                                            uint32_t slot, uint2 e, uint32_t warp, uint32_t nw) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t pos = 0;
+  for (uint32_t t = 0; t < P.ring; ++t) {  // ring slots in turn: rank = lanes below with slot t
+    const uint32_t m = __ballot_sync(0xffffffffu, alive && slot == t);
+    const uint32_t base = __shfl_sync(0xffffffffu, cnt, t);
+    if (slot == t) pos = base + __popc(m & ((1u << lane) - 1u));
+    if (lane == t) cnt += __popc(m);
+  }
+  if (alive) bucket_at(P, slot, warp, nw)[pos] = e;
+}
+
+// o / S for o < 2^31 (S = seg_bits >= 2^13): multiply-high, then one correction
+__device__ __forceinline__ uint32_t div_seg(const SieveParams &P, uint32_t o) {
+  uint32_t d = __umulhi(o, P.inv_seg);
+  if (d * P.seg_bits > o) --d;
+  return d;
+}
+
+// fill the warp's buckets at the start of its run: first hit of every owned
+// bucket prime at or after slot 0 of segment s0 (64-bit: the hit may lie far
+// ahead when p^2 is beyond the run start)
+__device__ __forceinline__ void bucket_fill(const SieveParams &P, const PrimeRegions &R,
+                                            uint32_t &cnt, uint64_t s0, uint64_t s1) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint64_t a = P.o0 + 2ull * s0 * P.seg_bits;  // first odd integer of the run
+  const uint64_t run = (s1 - s0) * (uint64_t)P.seg_bits;
+  for (uint32_t ib = R.big + warp; ib < R.end; ib += 32u * nw) {
+    const uint32_t i = ib + lane * nw;
+    bool alive = i < R.end;
+    uint32_t p = 0, slot = 0, o = 0;
+    if (alive) {
+      p = __ldg(P.primes + i);
+      const uint64_t pp = (uint64_t)p * p;
+      const uint64_t q = __umul64hi(a, __ldg(P.recips + i));
+      uint32_t r = (uint32_t)(a - q * (uint64_t)p);
+      r = min(r, r - p);
+      uint64_t d = r ? p - r : 0u;
+      d += (d & 1u) ? p : 0u;  // a odd: the next odd multiple is a + d, d even
+      uint64_t j = d >> 1;
+      if (a + 2ull * j < pp) j = (pp - a) >> 1;
+      alive = j < run;
+      if (alive) {
+        const uint64_t dseg = j / P.seg_bits;
+        const uint32_t dd = (uint32_t)min(dseg, (uint64_t)(P.ring - 1u));
+        o = (uint32_t)(j - (uint64_t)dd * P.seg_bits);
+        slot = (uint32_t)((s0 + dd) % P.ring);
+      }
+    }
+    bucket_push(P, cnt, alive, slot, make_uint2(p, o), warp, nw);
+  }
+}
+
+// drain the warp's ring slot of segment s: mark, then re-queue
+__device__ __forceinline__ void bucket_drain(const SieveParams &P, uint32_t &cnt, uint32_t sb,
+                                             uint32_t q, uint32_t left, uint32_t valid) {
+  // q = s mod R, left = s1 - s: no 64-bit division here (a runtime 64-bit
+  // modulo is a subroutine call, and ptxas then puts YIELDs in every loop of
+  // the kernel: measured 1.5x slower marking)
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t n = __shfl_sync(0xffffffffu, cnt, q);
+  const uint2 *src = bucket_at(P, q, warp, nw);
+  for (uint32_t e0 = 0; e0 < n; e0 += 32u * kDrainILP) {
+    uint2 v[kDrainILP];
+#pragma unroll
+    for (uint32_t u = 0; u < kDrainILP; ++u) {  // all loads first: their latency overlaps
+      const uint32_t e = e0 + 32u * u + lane;
+      v[u] = e < n ? __ldcg(src + e) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kDrainILP; ++u) {
+      const uint32_t p = v[u].x;
+      uint32_t o = v[u].y, slot = 0;
+      bool alive = e0 + 32u * u + lane < n;
+      if (alive) {
+        // the hits of this segment: p > S / kBucketHits, so at most
+        // kBucketHits of them (o >= S: an entry parked here, no hit)
+#pragma unroll
+        for (uint32_t h = 0; h < kBucketHits; ++h) {
+          if (o < valid) {
+            const uint32_t J = 4u * o + 32u * sb;
+            red_or(j_addr(J), j_mask(J));
+            o += p;
+          }
+        }
+        const uint32_t d = min(div_seg(P, o), P.ring - 1u);
+        o -= d * P.seg_bits;
+        alive = d >= 1u && d < left;
+        slot = q + d >= P.ring ? q + d - P.ring : q + d;
+      }
+      bucket_push(P, cnt, alive, slot, make_uint2(p, o), warp, nw);
+    }
+  }
+  if (lane == q) cnt = 0;  // no push above targets slot q (d >= 1)
 }
 
 // In-place 32x32 bit transpose of every 1024-slot block of the segment
@@ -532,10 +652,12 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
                                                 bool only_end) {
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t nb = *P.nbase;
-  if (warp < (only_end ? 1u : 4u)) {
+  if (warp < (only_end ? 1u : 5u)) {
     const uint64_t x = warp == 0 ? (uint64_t)r
                      : warp == 1 ? P.seg_bits / kUnitHits
-                     : warp == 2 ? P.seg_bits / kClassHits : P.seg_bits / kWarpHits;
+                     : warp == 2 ? P.seg_bits / kClassHits
+                     : warp == 3 ? P.seg_bits / kWarpHits
+                     : P.buckets ? P.seg_bits / kBucketHits : ~0ull;
     const uint32_t u = warp_upper_bound(P.primes, nb, x);
     if ((threadIdx.x & 31u) == 0) scratch[warp] = u;
   }
@@ -546,6 +668,7 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
     R.unit = max(R.start, min(R.end, scratch[1]));
     R.cls = max(R.unit, min(R.end, scratch[2]));
     R.warp = max(R.cls, min(R.end, scratch[3]));
+    R.big = max(R.warp, min(R.end, scratch[4]));
   }
 }
 
@@ -567,14 +690,27 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   __shared__ unsigned long long red[64];
   __shared__ PrimeRegions sR;
   __shared__ uint32_t s_last;
-  __shared__ uint32_t s_ub[4];
+  __shared__ uint32_t s_ub[5];
 
   for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
   compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
   __syncthreads();
 
   unsigned long long cnt = 0, sum = 0;
-  for (uint64_t s = blockIdx.x; s < P.nseg; s += gridDim.x) {
+  // segments round robin; with the buckets of step A5 a range is sieved in
+  // contiguous runs (the buckets carry each large prime from one segment of
+  // the run to the next)
+  const bool buckets = MODE != kBatch && P.buckets != nullptr && !(P.flags & kFlagSkipMarking);
+  const uint64_t s_begin = buckets ? blockIdx.x * P.nseg / gridDim.x : blockIdx.x;
+  const uint64_t s_end = buckets ? (blockIdx.x + 1ull) * P.nseg / gridDim.x : P.nseg;
+  const uint64_t s_step = buckets ? 1u : gridDim.x;
+  uint32_t bcnt = 0;  // lane t: fill count of the warp's bucket slot t
+  uint32_t bq = 0;    // ring slot of the current segment
+  if (buckets && s_begin < s_end) {
+    bucket_fill(P, sR, bcnt, s_begin, s_end);
+    bq = (uint32_t)(s_begin % P.ring);
+  }
+  for (uint64_t s = s_begin; s < s_end; s += s_step) {
     uint64_t a, bit0, o0;
     uint32_t valid;
     if (MODE == kBatch) {
@@ -593,6 +729,10 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
     if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, sR, a, valid, P.prof);
+    if (buckets) {
+      bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s), valid);
+      bq = bq + 1u == P.ring ? 0u : bq + 1u;
+    }
     __syncthreads();
     const long long c2 = P.prof ? clock64() : 0;
     if (MODE == kBatch) {

@@ -124,6 +124,7 @@ struct Ctx {
   DevBuf<uint64_t> list;
   DevBuf<sv::BatchItem> items;
   DevBuf<uint64_t> bres;
+  DevBuf<uint2> buckets;  // step A5 bucket rings
   uint64_t *h_res = nullptr;  // pinned [2]
   unsigned long long *prof = nullptr;  // diagnostics: phase-cycle counters
   uint32_t flags = 0;                  // diagnostics: sv::kFlagSkipMarking
@@ -290,11 +291,35 @@ sv::SieveParams params_for(const Plan &P, const uint32_t *primes, const uint64_t
   return sp;
 }
 
+// Step A5 (option buckets = 1): per-segment buckets for the primes with
+// fewer than kBucketHits hits per segment (p > S / kBucketHits), for a range
+// sieved in contiguous runs of segments per CTA.  Not in batch mode (one or
+// two segments per interval: nothing to skip), when no such prime exists, and
+// when a CTA's run exceeds 2^31 odd slots (bucket offsets are 32-bit).
+int setup_buckets(sv::SieveParams &sp, int grid) {
+  sp.buckets = nullptr;
+  if (g.opt.buckets != 1) return 0;
+  const uint64_t S = sp.seg_bits;
+  if ((uint64_t)sp.r <= S / sv::kBucketHits) return 0;
+  const uint64_t run = (sp.nseg + grid - 1) / grid * S;
+  if (run >= (1ull << 31)) return 0;
+  const uint64_t nw = g.opt.threads / 32;
+  const uint64_t capw = (base_capacity(sp.r) + nw - 1) / nw;
+  const uint64_t ring = std::min<uint64_t>(sv::kMaxRing, (sp.r + S - 1) / S + 2);
+  TRY(g.buckets.ensure((size_t)grid * ring * nw * capw));
+  sp.buckets = g.buckets.p;
+  sp.ring = (uint32_t)ring;
+  sp.capw = (uint32_t)capw;
+  sp.inv_seg = (uint32_t)(((1ull << 32) + S - 1) / S);
+  return 0;
+}
+
 int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork) {
   TRY(ensure_smem_attr());
   const int grid = grid_for(nwork);
   TRY(g.partials.ensure(2 * (size_t)grid));
   sp.partials = g.partials.p;
+  if (mode != sv::kBatch) TRY(setup_buckets(sp, grid));
   const int ng = ng_for_wheel(g.opt.wheel);
   CUDA_TRY(sv::launch_sieve(ng, mode, sp, grid, (int)g.opt.threads, sieve_smem(), g.stream()));
   g_launches += 1;
@@ -592,8 +617,10 @@ int sieve_set_options(const sieve_options *o) {
   sieve_options n;
   default_options(n);
   if (o) {
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 3; ++i)
       if (o->reserved[i]) return fail(SIEVE_EINVAL, "reserved option fields must be zero");
+    if (o->buckets > 1) return fail(SIEVE_EINVAL, "buckets %u not in {0, 1}", o->buckets);
+    n.buckets = o->buckets;
     if (o->segment_kb) {
       if (o->segment_kb < 4 || o->segment_kb > 224)
         return fail(SIEVE_EINVAL, "segment_kb %u is not in [4, 224]", o->segment_kb);
@@ -637,6 +664,7 @@ void sieve_shutdown(void) {
   g.tables.release(); g.primes.release(); g.recips.release(); g.nbase.release();
   g.partials.release(); g.done.release(); g.result.release(); g.bitmap.release();
   g.segcnt.release(); g.segoff.release(); g.list.release(); g.items.release(); g.bres.release();
+  g.buckets.release();
   if (g.h_res) cudaFreeHost(g.h_res);
   g.h_res = nullptr;
   if (g.own) cudaStreamDestroy(g.own);

@@ -218,3 +218,36 @@ def test_config5_batch_digest_and_samples():
     idx = np.array([0, 1, 2, 3, 4095] + list(range(7, 4096, 409)))
     oc, os_ = oracle.batch(lo[idx], hi[idx])
     assert np.array_equal(c[idx], oc) and np.array_equal(s[idx], os_)
+
+
+# ------------------------------------------------- step A5: bucket path
+@pytest.mark.parametrize("seg_kb", [4, 8, 32])
+@pytest.mark.parametrize("buckets", [0, 1])
+def test_bucket_path_vs_oracle(seg_kb, buckets):
+    """Large primes (p > S) through per-segment buckets (buckets=1) and
+    through per-segment Barrett first hits (buckets=0) agree with the oracle:
+    ranges from 2 (p^2 inside the run: entries parked ahead), windows at
+    10^12 (p up to 10^6 > 30 S at 4 KiB: the ring clamps at 32), ragged
+    ends, and bitmap/list outputs."""
+    sv.set_options(segment_kb=seg_kb, buckets=buckets)
+    assert sv.get_options()["buckets"] == buckets
+    cases = [(2, 3 * 10**8), (10**12 - 7, 10**12 + 2 * 10**7 + 3),
+             (999_999_999_989, 1_000_000_031_000)]
+    cases += inputs.random_intervals(4, seed=20 + seg_kb, lo_max=10**12, width_max=10**7)
+    for lo, hi in cases:
+        assert sv.stats(lo, hi) == oracle.stats(lo, hi), (lo, hi)
+    lo, hi = 10**12 - 7, 10**12 + 3 * 10**6 + 3
+    bm, c = sv.bitmap(lo, hi)
+    obm, oc, _ = oracle.bitmap(lo, hi)
+    assert c == oc and np.array_equal(bm, obm)
+    lst, c2 = sv.primes(lo, hi)
+    assert c2 == oc and np.array_equal(lst, oracle.primes(lo, hi))
+
+
+def test_bucket_path_config4_full_window():
+    """Config 4 with the bucket path carrying 71% of the base primes (32 KiB
+    segments) and with the default segment, against the pinned values."""
+    lo, hi = inputs.CONFIG4
+    for seg_kb, buckets in ((32, 1), (32, 0), (64, 1)):
+        sv.set_options(segment_kb=seg_kb, buckets=buckets)
+        assert sv.stats(lo, hi) == (int(PINS["config4.count"]), int(PINS["config4.sum"]))
