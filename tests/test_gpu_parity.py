@@ -251,3 +251,32 @@ def test_bucket_path_config4_full_window():
     for seg_kb, buckets in ((32, 1), (32, 0), (64, 1)):
         sv.set_options(segment_kb=seg_kb, buckets=buckets)
         assert sv.stats(lo, hi) == (int(PINS["config4.count"]), int(PINS["config4.sum"]))
+
+
+def test_config4_full_list_on_device_subwindows():
+    """Config 4 at full size, as the benchmark runs it: the whole prime list
+    of [10^12, 10^12 + 10^10) compacted into device memory (361,840,208 u64,
+    2.9 GB), then the 16 seeded sub-windows (reading R12) sliced out of it by
+    binary search and compared with their pinned count / sum / list FNV, and
+    sub-window 0 element by element with the oracle.  Whole-list properties:
+    count, sum mod 2^64, strictly ascending, all odd."""
+    import torch
+    lo, hi = inputs.CONFIG4
+    n = int(PINS["config4.count"])
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    _, c = sv.primes(lo, hi, cap=n, out=out)
+    assert c == n
+    assert int(out.sum().item()) & MASK64 == int(PINS["config4.sum"])
+    assert bool((out[1:] > out[:-1]).all()) and bool((out & 1).all())
+    assert int(out[0]) >= lo and int(out[-1]) < hi
+    for k, (s, cnt, sm, h) in enumerate(subwindows()):
+        b = torch.tensor([s, s + 10**7], dtype=torch.int64, device="cuda")
+        i0, i1 = torch.searchsorted(out, b).tolist()
+        sl = out[i0:i1].cpu().numpy().astype(np.uint64)
+        assert sl.size == cnt
+        assert int(sl.sum(dtype=np.uint64)) == sm
+        assert oracle.fnv1a64(sl.astype("<u8")) == h
+        if k == 0:
+            assert np.array_equal(sl, oracle.primes(s, s + 10**7))
+    del out
+    torch.cuda.empty_cache()
