@@ -152,7 +152,9 @@ cudaError_t launch_sieve(int ng, int mode, const SieveParams &p, int grid, int t
                          size_t smem, cudaStream_t s);
 cudaError_t set_sieve_smem_limits(size_t smem);
 cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64_t *recips,
-                               uint32_t cap, uint32_t *nbase, cudaStream_t s);
+                               uint32_t cap, uint32_t *nbase, uint64_t *flags, uint32_t epoch,
+                               int nsm, cudaStream_t s);
+uint32_t base_slices(uint32_t r);  // look-back flags the base-prime kernel needs
 cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
                            uint32_t cap, cudaStream_t s);
 cudaError_t launch_scan_segments(const uint32_t *seg_counts, uint64_t nseg, uint64_t *seg_off,

@@ -53,6 +53,20 @@ __device__ __forceinline__ uint32_t first_hit(uint64_t a, uint64_t seg_end, uint
   return pp >= seg_end ? kNone : j;
 }
 
+// floor((2^64-1)/p) for an odd p >= 3, without a 64-bit integer division:
+// a double quotient (within 2^12 of the result), then the exact remainder
+// T = (2^64-1) - q p (|T| < 2^40, so mod-2^64 arithmetic gives it as a signed
+// number) corrects q by floor(T / p), with a final +-1 guard on the rounding.
+__device__ __forceinline__ uint64_t recip_of(uint32_t p) {
+  uint64_t q = __double2ull_rz(1.8446744073709552e19 / (double)p);
+  int64_t T = (int64_t)(~0ull - q * (uint64_t)p);
+  int64_t d = (int64_t)floor((double)T / (double)p);
+  T -= d * (int64_t)p;
+  if (T < 0) { --d; T += p; }
+  if (T >= (int64_t)p) ++d;
+  return q + (uint64_t)d;
+}
+
 __device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t *v, uint32_t n, uint64_t x) {
   uint32_t lo = 0, hi = n;  // first index with v[idx] > x
   while (lo < hi) {
@@ -803,123 +817,148 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
 }
 
 // ---------------------------------------------------------------------------
-// A2: base primes.  One CTA: odd primes <= rs = isqrt(r) by trial division,
-// then the odd numbers <= r are sieved in shared-memory chunks and compacted
-// in order (block scan of per-thread counts).  Also writes the Barrett
-// reciprocal of every prime.
+// A2: base primes, the odd primes <= r (r <= 2^24), ascending, with their
+// Barrett reciprocals.  The odd numbers <= r are cut into slices of
+// kSliceBits; a CTA of kBaseThreads threads takes slices b, b + G, ... (all
+// CTAs resident).  Per slice: the odd primes q <= sqrt(r) (computed once per
+// CTA by trial division, kept in shared memory) mark their odd multiples
+// >= q^2 in a shared bitmap (thread t owns word t); the block counts the
+// survivors, publishes the slice's count, and finds the slice's place in the
+// list by a decoupled look-back over the earlier slices' published counts
+// (flags tagged with the launch's epoch, so no reset between launches); then
+// the primes are written in order (block scan of the per-thread counts).
 // ---------------------------------------------------------------------------
-constexpr uint32_t kBaseChunkBits = 1u << 19;  // 64 KiB of shared memory
-constexpr uint32_t kMaxSmall = 1024;           // odd primes <= 4096 number 563
+constexpr uint32_t kBaseThreads = 256;
+constexpr uint32_t kSliceBits = 32u * kBaseThreads;  // one word per thread
+constexpr uint32_t kMaxSmall = 1024;                 // odd primes <= 4096 number 563
+constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;
 
-__global__ void __launch_bounds__(1024, 1) k_base_primes(uint32_t r, uint32_t rs, uint32_t *primes,
-                                                         uint64_t *recips, uint32_t cap,
-                                                         uint32_t *nbase) {
-  extern __shared__ __align__(16) uint32_t bm[];  // kBaseChunkBits / 32 words
+__device__ __forceinline__ uint64_t make_flag(uint32_t epoch, uint64_t v, uint64_t st) {
+  return ((uint64_t)epoch << 48) | (v << 2) | st;
+}
+
+__global__ void __launch_bounds__(kBaseThreads) k_base_primes(uint32_t r, uint32_t rs, uint32_t *primes,
+                                                              uint64_t *recips, uint32_t cap,
+                                                              uint32_t *nbase, uint64_t *flags,
+                                                              uint32_t epoch) {
+  __shared__ uint32_t bm[kSliceBits / 32];
   __shared__ uint32_t sp[kMaxSmall];
-  __shared__ uint32_t s_wsum[32];
-  __shared__ uint32_t s_nsp, s_total;
-  const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31u, warp = tid >> 5;
-  const uint32_t nw = nt >> 5;
-  if (tid == 0) { s_nsp = 0; s_total = 0; }
+  __shared__ uint32_t s_j0[kMaxSmall];
+  __shared__ uint32_t s_w[kBaseThreads / 32];
+  __shared__ uint32_t s_nsp;
+  __shared__ unsigned long long s_off;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) s_nsp = 0;
   __syncthreads();
-
-  // small odd primes q <= rs, in ascending order: rounds of nt candidates
-  for (uint32_t base = 3; base <= rs; base += 2 * nt) {
-    const uint32_t q = base + 2 * tid;
+  // odd primes q <= rs, ascending: rounds of blockDim candidates, ballot compaction
+  for (uint32_t base = 3; base <= rs; base += 2u * blockDim.x) {
+    const uint32_t q = base + 2u * tid;
     bool isp = q <= rs;
     for (uint32_t d = 3; isp && d * d <= q; d += 2)
       if (q % d == 0) isp = false;
     const uint32_t bal = __ballot_sync(0xffffffffu, isp);
-    if (lane == 0) s_wsum[warp] = __popc(bal);
+    if (lane == 0) s_w[warp] = __popc(bal);
     __syncthreads();
     uint32_t off = s_nsp;
-    for (uint32_t w = 0; w < warp; ++w) off += s_wsum[w];
+    for (uint32_t w = 0; w < warp; ++w) off += s_w[w];
     off += __popc(bal & ((1u << lane) - 1u));
     if (isp && off < kMaxSmall) sp[off] = q;
     __syncthreads();
     if (tid == 0) {
       uint32_t t = 0;
-      for (uint32_t w = 0; w < nw; ++w) t += s_wsum[w];
+      for (uint32_t w = 0; w < nw; ++w) t += s_w[w];
       s_nsp += t;
     }
     __syncthreads();
   }
   const uint32_t nsp = min(s_nsp, kMaxSmall);
 
-  // odd n = 2i+1 for i in [1, imax]; chunk [i0, i0 + kBaseChunkBits)
+  // odd n = 2i + 1, i in [1, imax]; slice k covers i in [1 + k S, 1 + (k+1) S)
   const uint32_t imax = r >= 3 ? (r - 1) / 2 : 0;
-  for (uint32_t i0 = 1; i0 <= imax; i0 += kBaseChunkBits) {
-    const uint32_t nbits = min(kBaseChunkBits, imax - i0 + 1);
-    const uint32_t nwords = (nbits + 31) / 32;
-    for (uint32_t w = tid; w < nwords; w += nt) bm[w] = 0;
-    __syncthreads();
-    const uint32_t a = 2u * i0 + 1u;  // odd integer of bit 0 (r <= 2^24: 32-bit math)
-    const uint32_t e = a + 2u * nbits;
-    // every thread of the CTA on one small prime at a time (the tiny primes
-    // carry most of the marks; a warp per prime would serialise on q = 3)
-    for (uint32_t k = 0; k < nsp; ++k) {
-      const uint32_t q = sp[k];
-      const uint32_t qq = q * q;
-      if (qq >= e) break;
-      uint32_t m = qq;
-      if (m < a) {
-        m = ((a + q - 1u) / q) * q;
-        if (!(m & 1u)) m += q;
+  const uint32_t nslice = (imax + kSliceBits - 1) / kSliceBits;
+  for (uint32_t k = blockIdx.x; k < nslice; k += gridDim.x) {
+    const uint32_t i0 = 1 + k * kSliceBits;
+    const uint32_t nbits = min(kSliceBits, imax - i0 + 1);
+    bm[tid] = 0;
+    const uint32_t a = 2u * i0 + 1u, e = a + 2u * nbits;  // odd integers [a, e)
+    // the slice offset of every small prime's first odd multiple >= max(q^2, a),
+    // one prime per thread (the divisions run in parallel, not in the loop below)
+    for (uint32_t m = tid; m < nsp; m += blockDim.x) {
+      const uint32_t q = sp[m];
+      uint32_t f = q * q;
+      if (f < a) {
+        f = ((a + q - 1u) / q) * q;
+        if (!(f & 1u)) f += q;
       }
-      for (uint32_t j = (m - a) / 2u + tid * q; j < nbits; j += nt * q)
-        atomicOr(&bm[j >> 5], 1u << (j & 31));
+      s_j0[m] = f < e ? (f - a) / 2u : kNone;
     }
     __syncthreads();
-    // compaction: thread t owns words [t*wpt, (t+1)*wpt)
-    const uint32_t wpt = (nwords + nt - 1) / nt;
-    const uint32_t wb = tid * wpt, we = min(nwords, wb + wpt);
-    uint32_t c = 0;
-    for (uint32_t w = wb; w < we; ++w) {
-      uint32_t x = ~bm[w];
-      if (w == nwords - 1 && (nbits & 31)) x &= (1u << (nbits & 31)) - 1u;
-      c += __popc(x);
+    for (uint32_t m = 0; m < nsp; ++m) {  // all threads on one prime at a time
+      const uint32_t j0 = s_j0[m];
+      if (j0 == kNone) break;             // q^2 past the slice: so for every later prime
+      const uint32_t q = sp[m];
+      for (uint32_t j = j0 + tid * q; j < nbits; j += blockDim.x * q) atomicOr(&bm[j >> 5], 1u << (j & 31));
     }
-    // block exclusive scan of c
+    __syncthreads();
+    uint32_t x = ~bm[tid];
+    const uint32_t vb = nbits > 32u * tid ? nbits - 32u * tid : 0u;  // valid bits of word tid
+    if (vb < 32u) x &= (1u << vb) - 1u;
+    const uint32_t c = __popc(x);
     uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= (uint32_t)o) incl += y;
     }
-    if (lane == 31) s_wsum[warp] = incl;
+    if (lane == 31) s_w[warp] = incl;
     __syncthreads();
-    uint32_t off = s_total + incl - c;
-    for (uint32_t w = 0; w < warp; ++w) off += s_wsum[w];
-    for (uint32_t w = wb; w < we; ++w) {
-      uint32_t x = ~bm[w];
-      if (w == nwords - 1 && (nbits & 31)) x &= (1u << (nbits & 31)) - 1u;
-      while (x) {
-        const uint32_t b = __ffs(x) - 1;
-        x &= x - 1;
-        const uint32_t p = (uint32_t)(a + 2ull * (32ull * w + b));
-        if (off < cap) {
-          primes[off] = p;
-          recips[off] = ~0ull / p;
+    uint32_t excl = incl - c, tot = 0;
+    for (uint32_t w = 0; w < nw; ++w) {
+      if (w < warp) excl += s_w[w];
+      tot += s_w[w];
+    }
+    if (tid == 0) {  // publish, then look back for the slice's offset
+      volatile unsigned long long *fl = reinterpret_cast<volatile unsigned long long *>(flags);
+      if (k == 0) {
+        fl[0] = make_flag(epoch, tot, kFlagIncl);
+        s_off = 0;
+      } else {
+        fl[k] = make_flag(epoch, tot, kFlagAgg);
+        uint64_t pre = 0;
+        for (uint32_t j = k; j-- > 0;) {
+          uint64_t f;
+          do { f = fl[j]; } while ((f >> 48) != epoch);  // not yet published in this launch
+          pre += (f >> 2) & ((1ull << 46) - 1);
+          if ((f & 3u) == kFlagIncl) break;
         }
-        ++off;
+        __threadfence();
+        fl[k] = make_flag(epoch, pre + tot, kFlagIncl);
+        s_off = pre;
       }
+      if (k == nslice - 1) *nbase = (uint32_t)min((uint64_t)cap, (uint64_t)(s_off + tot));
     }
     __syncthreads();
-    if (tid == 0) {
-      uint32_t t = 0;
-      for (uint32_t w = 0; w < nw; ++w) t += s_wsum[w];
-      s_total += t;
+    uint64_t o = s_off + excl;
+    while (x) {
+      const uint32_t b = __ffs(x) - 1;
+      x &= x - 1;
+      const uint32_t p = a + 2u * (32u * tid + b);
+      if (o < cap) {
+        primes[o] = p;
+        recips[o] = recip_of(p);
+      }
+      ++o;
     }
-    __syncthreads();
+    __syncthreads();  // bm and s_w are reused by the next slice
   }
-  if (tid == 0) *nbase = min(s_total, cap);
+  if (nslice == 0 && blockIdx.x == 0 && tid == 0) *nbase = 0;
 }
 
 __global__ void k_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
                           uint32_t cap) {
   const uint32_t n = min(*nbase, cap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    recips[i] = ~0ull / primes[i];
+    recips[i] = recip_of(primes[i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -957,12 +996,24 @@ __global__ void __launch_bounds__(1024) k_scan_segments(const uint32_t *seg_coun
   }
 }
 
-__global__ void __launch_bounds__(1024) k_compact(const uint32_t *__restrict__ bitmap, uint64_t nbits,
-                                                  uint64_t o0, uint32_t seg_bits, uint64_t nseg,
-                                                  const uint64_t *__restrict__ seg_off,
-                                                  uint32_t add_two, uint64_t *__restrict__ out,
-                                                  uint64_t cap) {
+// Pieces of kPieceWords bitmap words: every thread takes kCompactWPT
+// consecutive words, a block scan of the per-thread prime counts gives each
+// thread its place, the primes are expanded into a shared-memory staging
+// area in list order and the block copies the staging area to the list with
+// coalesced stores (consecutive threads, consecutive u64).  A piece with
+// more primes than the staging area holds (only for small integers, where
+// primes are dense) is written straight from the registers instead.
+constexpr uint32_t kCompactThreads = 1024;
+constexpr uint32_t kCompactWPT = 2;  // words per thread per piece
+constexpr uint32_t kPieceWords = kCompactThreads * kCompactWPT;
+constexpr uint32_t kStage = 8192;    // staged primes per piece (64 KiB)
+
+__global__ void __launch_bounds__(kCompactThreads) k_compact(
+    const uint32_t *__restrict__ bitmap, uint64_t nbits, uint64_t o0, uint32_t seg_bits, uint64_t nseg,
+    const uint64_t *__restrict__ seg_off, uint32_t add_two, uint64_t *__restrict__ out, uint64_t cap) {
+  extern __shared__ __align__(16) unsigned long long stage[];  // kStage
   __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_tot;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x >> 5;
   if (add_two && blockIdx.x == 0 && tid == 0 && cap > 0) out[0] = 2;
   const uint64_t words = (nbits + 31) / 32;
@@ -972,12 +1023,21 @@ __global__ void __launch_bounds__(1024) k_compact(const uint32_t *__restrict__ b
     if (off >= cap) continue;  // everything here lands past the cap
     const uint64_t wb = s * seg_words;
     const uint64_t we = min(words, wb + seg_words);
-    for (uint64_t w0 = wb; w0 < we; w0 += blockDim.x) {
-      const uint64_t w = w0 + tid;
-      const uint32_t x = w < we ? __ldg(bitmap + w) : 0u;
-      const uint32_t c = __popc(x);
-      const uint32_t bal_incl = c;
-      uint32_t incl = bal_incl;
+    for (uint64_t w0 = wb; w0 < we; w0 += kPieceWords) {
+      // this thread's words (w0 + 2 tid, w0 + 2 tid + 1), zero past the end
+      const uint64_t w = w0 + kCompactWPT * tid;
+      uint32_t x[kCompactWPT];
+      if (w + 1 < we) {
+        const uint2 v = __ldcs(reinterpret_cast<const uint2 *>(bitmap + w));  // 8-byte aligned: w even
+        x[0] = v.x;
+        x[1] = v.y;
+      } else {
+        x[0] = w < we ? __ldcs(bitmap + w) : 0u;
+        x[1] = 0u;
+      }
+      const uint32_t c = __popc(x[0]) + __popc(x[1]);
+      // block exclusive scan of c
+      uint32_t incl = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -985,21 +1045,50 @@ __global__ void __launch_bounds__(1024) k_compact(const uint32_t *__restrict__ b
       }
       if (lane == 31) s_w[warp] = incl;
       __syncthreads();
-      uint64_t my = off + incl - c;
-      uint32_t tot = 0;
-      for (uint32_t k = 0; k < nw; ++k) {
-        if (k < warp) my += s_w[k];
-        tot += s_w[k];
+      if (warp == 0) {
+        uint32_t t = lane < nw ? s_w[lane] : 0u, ti = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+          if (lane >= (uint32_t)o) ti += y;
+        }
+        if (lane < nw) s_w[lane] = ti - t;  // exclusive warp offsets
+        if (lane == 31) s_tot = ti;
       }
-      uint32_t y = x;
-      while (y) {
-        const uint32_t b = __ffs(y) - 1;
-        y &= y - 1;
-        if (my < cap) out[my] = o0 + 2ull * (32ull * w + b);
-        ++my;
+      __syncthreads();
+      const uint32_t my = s_w[warp] + incl - c, tot = s_tot;
+      if (tot <= kStage) {
+        uint32_t k = my;
+#pragma unroll
+        for (uint32_t u = 0; u < kCompactWPT; ++u) {
+          uint32_t y = x[u];
+          const uint64_t base = o0 + 64ull * (w + u);
+          while (y) {
+            const uint32_t b = __ffs(y) - 1;
+            y &= y - 1;
+            stage[k++] = base + 2ull * b;
+          }
+        }
+        __syncthreads();
+        const uint64_t room = cap > off ? cap - off : (uint64_t)0;
+        const uint64_t n = (uint64_t)tot < room ? (uint64_t)tot : room;
+        for (uint32_t i = tid; i < n; i += blockDim.x) __stcs(out + off + i, stage[i]);
+      } else {
+        uint64_t k = off + my;
+#pragma unroll
+        for (uint32_t u = 0; u < kCompactWPT; ++u) {
+          uint32_t y = x[u];
+          const uint64_t base = o0 + 64ull * (w + u);
+          while (y) {
+            const uint32_t b = __ffs(y) - 1;
+            y &= y - 1;
+            if (k < cap) out[k] = base + 2ull * b;
+            ++k;
+          }
+        }
       }
       off += tot;
-      __syncthreads();
+      __syncthreads();  // stage and s_w are reused by the next piece
     }
   }
 }
@@ -1053,8 +1142,10 @@ cudaError_t set_sieve_smem_limits(size_t smem) {
   if ((e = set_attr_ng<4>(smem))) return e;
   if ((e = set_attr_ng<5>(smem))) return e;
   if ((e = set_attr_ng<6>(smem))) return e;
-  return cudaFuncSetAttribute(k_base_primes, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(kBaseChunkBits / 8));
+  if ((e = cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kStage * 8))))
+    return e;
+  return cudaSuccess;
 }
 
 template <int NG, int MODE>
@@ -1070,9 +1161,18 @@ int sieve_max_ctas_per_sm(int ng, int mode, int threads, size_t smem) {
   return occ_t<4, kCount>(threads, smem);
 }
 
+uint32_t base_slices(uint32_t r) {
+  const uint32_t imax = r >= 3 ? (r - 1) / 2 : 0;
+  return (imax + kSliceBits - 1) / kSliceBits;
+}
+
 cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64_t *recips,
-                               uint32_t cap, uint32_t *nbase, cudaStream_t s) {
-  k_base_primes<<<1, 1024, kBaseChunkBits / 8, s>>>(r, rs, primes, recips, cap, nbase);
+                               uint32_t cap, uint32_t *nbase, uint64_t *flags, uint32_t epoch,
+                               int nsm, cudaStream_t s) {
+  const uint32_t ns = base_slices(r);
+  // all CTAs resident (the look-back waits on earlier slices): <= 4 per SM
+  const uint32_t grid = ns < 4u * (uint32_t)nsm ? (ns ? ns : 1u) : 4u * (uint32_t)nsm;
+  k_base_primes<<<grid, kBaseThreads, 0, s>>>(r, rs, primes, recips, cap, nbase, flags, epoch);
   return cudaGetLastError();
 }
 
@@ -1092,9 +1192,10 @@ cudaError_t launch_scan_segments(const uint32_t *seg_counts, uint64_t nseg, uint
 cudaError_t launch_compact(const uint32_t *bitmap, uint64_t nbits, uint64_t o0, uint32_t seg_bits,
                            uint64_t nseg, const uint64_t *seg_off, uint32_t add_two, uint64_t *out,
                            uint64_t cap, cudaStream_t s) {
-  int grid = nseg < 148 * 8 ? (int)nseg : 148 * 8;
+  int grid = nseg < 148 * 2 ? (int)nseg : 148 * 2;  // 2 x (64 KiB staging + 1024 threads) per SM
   if (grid < 1) grid = 1;
-  k_compact<<<grid, 1024, 0, s>>>(bitmap, nbits, o0, seg_bits, nseg, seg_off, add_two, out, cap);
+  k_compact<<<grid, kCompactThreads, kStage * 8, s>>>(bitmap, nbits, o0, seg_bits, nseg, seg_off,
+                                                     add_two, out, cap);
   return cudaGetLastError();
 }
 

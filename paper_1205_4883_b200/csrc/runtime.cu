@@ -125,6 +125,8 @@ struct Ctx {
   DevBuf<sv::BatchItem> items;
   DevBuf<uint64_t> bres;
   DevBuf<uint2> buckets;  // step A5 bucket rings
+  DevBuf<uint64_t> kflags;  // K1 look-back flags (epoch-tagged, never reset)
+  uint32_t epoch = 0;
   uint64_t *h_res = nullptr;  // pinned [2]
   unsigned long long *prof = nullptr;  // diagnostics: phase-cycle counters
   uint32_t flags = 0;                  // diagnostics: sv::kFlagSkipMarking
@@ -257,7 +259,19 @@ int base_primes(uint64_t r, uint32_t *primes, uint64_t *recips, uint64_t cap, ui
   if (r > (1ull << 24)) return fail(SIEVE_ERANGE, "base-prime bound %llu > 2^24", (unsigned long long)r);
   const uint32_t rs = (uint32_t)isqrt_u64(r);
   TRY(ensure_smem_attr());
-  CUDA_TRY(sv::launch_base_primes((uint32_t)r, rs, primes, recips, (uint32_t)cap, nbase, s));
+  const uint32_t ns = sv::base_slices((uint32_t)r);
+  if (ns > g.kflags.n) {
+    TRY(g.kflags.ensure(ns));
+    CUDA_TRY(cudaMemsetAsync(g.kflags.p, 0, g.kflags.n * sizeof(uint64_t), s));
+    g.epoch = 0;
+  }
+  g.epoch = (g.epoch + 1) & 0xFFFF;
+  if (g.epoch == 0) {  // 2^16 launches: clear stale tags once
+    CUDA_TRY(cudaMemsetAsync(g.kflags.p, 0, g.kflags.n * sizeof(uint64_t), s));
+    g.epoch = 1;
+  }
+  CUDA_TRY(sv::launch_base_primes((uint32_t)r, rs, primes, recips, (uint32_t)cap, nbase,
+                                  g.kflags.p ? g.kflags.p : nullptr, g.epoch, g.nsm, s));
   g_launches += 1;
   return 0;
 }
@@ -664,7 +678,7 @@ void sieve_shutdown(void) {
   g.tables.release(); g.primes.release(); g.recips.release(); g.nbase.release();
   g.partials.release(); g.done.release(); g.result.release(); g.bitmap.release();
   g.segcnt.release(); g.segoff.release(); g.list.release(); g.items.release(); g.bres.release();
-  g.buckets.release();
+  g.buckets.release(); g.kflags.release();
   if (g.h_res) cudaFreeHost(g.h_res);
   g.h_res = nullptr;
   if (g.own) cudaStreamDestroy(g.own);

@@ -120,6 +120,39 @@ def config4(seg_kb):
     sv.set_options()
 
 
+def config4_list(seg_kb=0):
+    """Config 4 prime list (361,840,208 u64 = 2.9 GB) compacted into device
+    memory through sieve_primes (synchronous call: base primes, bitmap-mode
+    sieve into scratch, segment scan, compaction, count read-back)."""
+    if seg_kb:
+        sv.set_options(segment_kb=seg_kb)
+    lo, hi = inputs.CONFIG4
+    n = 361840208
+    out = torch.empty(n, dtype=torch.int64, device=dev)
+
+    def run():
+        return sv.primes(lo, hi, cap=n, out=out)[1]
+    for _ in range(2):
+        c = run()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        run()
+        ts.append(time.perf_counter() - t0)
+    med = statistics.median(ts)
+    emit({"config": 4, "mode": "list (sieve_primes, device out, synchronous call)",
+          "segment_kb": sv.get_options()["segment_kb"], "ms": med * 1e3, "ok": c == n,
+          "integers_per_s": (hi - lo) / med, "list_bytes": n * 8, "list_gbs": n * 8 / med / 1e9,
+          "list_hbm_frac": n * 8 / med / 1e9 / HBM_PEAK})
+    del out
+    torch.cuda.empty_cache()
+    sv.set_options()
+
+
 def config5():
     lo, hi = inputs.config5_intervals()
     total = int((hi - lo).sum())
@@ -150,5 +183,6 @@ if __name__ == "__main__":
     if "4" in which:
         for kb in (32, 208):
             config4(kb)
+        config4_list()
     if "5" in which:
         config5()
