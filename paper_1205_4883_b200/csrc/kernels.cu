@@ -132,29 +132,32 @@ struct WheelGroup {
 };
 
 // OR the table words of groups G..NG-1 for the current segment word and
-// advance their indices (compile-time recursion: constant moduli).
+// advance their indices (compile-time recursion: constant moduli).  Indices
+// are byte offsets ig = 4 y; the step d4 = 4 (32 nt mod P) is applied mod 4P
+// as ig' = umin(ig + d4, ig - e4), e4 = 4P - d4 (ig - e4 wraps above every
+// valid offset when ig < e4): one add and one add+min per group and word.
 template <int G, int NG>
-__device__ __forceinline__ uint32_t wheel_word(const uint32_t *tab, uint32_t (&ig)[NG],
-                                               const uint32_t (&dg)[NG]) {
+__device__ __forceinline__ uint32_t wheel_word(const char *tabb, uint32_t (&ig)[NG],
+                                               const uint32_t (&d4)[NG], const uint32_t (&e4)[NG]) {
   if constexpr (G == NG) {
     return 0u;
   } else {
-    constexpr uint32_t P = WheelGroup<G>::P;
-    const uint32_t v = tab[WheelGroup<G>::OFF + ig[G]];
-    const uint32_t x = ig[G] + dg[G];
-    ig[G] = min(x, x - P);  // x < 2P: x - P wraps above x when x < P
-    return v | wheel_word<G + 1, NG>(tab, ig, dg);
+    const uint32_t v = *reinterpret_cast<const uint32_t *>(tabb + 4u * WheelGroup<G>::OFF + ig[G]);
+    const uint32_t t = ig[G] - e4[G];
+    ig[G] = min(ig[G] + d4[G], t);
+    return v | wheel_word<G + 1, NG>(tabb, ig, d4, e4);
   }
 }
 
 template <int G, int NG>
-__device__ __forceinline__ void wheel_setup(uint32_t (&ig)[NG], uint32_t (&dg)[NG], uint64_t X0,
-                                            uint32_t tid, uint32_t nt) {
+__device__ __forceinline__ void wheel_setup(uint32_t (&ig)[NG], uint32_t (&d4)[NG], uint32_t (&e4)[NG],
+                                            uint64_t X0, uint32_t tid, uint32_t nt) {
   if constexpr (G < NG) {
     constexpr uint32_t P = WheelGroup<G>::P;
-    ig[G] = (uint32_t)((X0 % P + 1024u * (tid >> 5) + (tid & 31u)) % P);
-    dg[G] = (32u * nt) % P;
-    wheel_setup<G + 1, NG>(ig, dg, X0, tid, nt);
+    ig[G] = 4u * (uint32_t)((X0 % P + 1024u * (tid >> 5) + (tid & 31u)) % P);
+    d4[G] = 4u * ((32u * nt) % P);
+    e4[G] = 4u * P - d4[G];
+    wheel_setup<G + 1, NG>(ig, d4, e4, X0, tid, nt);
   }
 }
 
@@ -163,18 +166,19 @@ __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, u
                                            uint64_t bit0, uint32_t valid, uint64_t a) {
   const uint32_t nt = blockDim.x, tid = threadIdx.x;
   const uint32_t nwords = ((valid + 1023u) >> 10) << 5;
-  uint32_t ig[NG], dg[NG];
-  wheel_setup<0, NG>(ig, dg, ((o0 - 1) >> 1) + bit0, tid, nt);
+  uint32_t ig[NG], d4[NG], e4[NG];
+  wheel_setup<0, NG>(ig, d4, e4, ((o0 - 1) >> 1) + bit0, tid, nt);
+  const char *tabb = reinterpret_cast<const char *>(tab);
   // fast path: words of whole blocks with no fix-up (block 0 holds the
   // integers <= w when a <= w) and no tail slot
   const uint32_t wfast_lo = a <= wheel_bound(NG) ? 32u : 0u;
   const uint32_t wfast_hi = (valid >> 10) << 5;
   uint32_t w = tid;
   if (wfast_lo == 0) {
-    for (; w < wfast_hi; w += nt) seg[w] = wheel_word<0, NG>(tab, ig, dg);
+    for (; w < wfast_hi; w += nt) seg[w] = wheel_word<0, NG>(tabb, ig, d4, e4);
   }
   for (; w < nwords; w += nt) {
-    uint32_t v = wheel_word<0, NG>(tab, ig, dg);
+    uint32_t v = wheel_word<0, NG>(tabb, ig, d4, e4);
     const uint32_t b = w & 31u, j0 = ((w >> 5) << 10) + b;  // slot of the word's bit 0
     if (w < 32u) {  // bit 0 <-> n = a + 2b (a <= w: n <= 2w+63, bits >= 1 are > w)
       const uint64_t n = a + 2ull * b;
