@@ -144,6 +144,9 @@ struct SieveParams {
 // measure the bitmap write-back stage in isolation.  Results are then wrong
 // by design; never set on the product path.
 constexpr uint32_t kFlagSkipMarking = 1u;
+// Diagnostic flags: skip marking regions (A1+A2), (B), (C) -- marginal cost
+// of each region in context.  Wrong results by design.
+constexpr uint32_t kFlagSkipA = 2u, kFlagSkipB = 4u, kFlagSkipC = 8u;
 
 enum Mode { kCount = 0, kBitmap = 1, kBatch = 2 };
 

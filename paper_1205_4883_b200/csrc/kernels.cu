@@ -253,8 +253,13 @@ __device__ __forceinline__ uint32_t class_limit(uint32_t j, uint32_t valid) {
 // i mod nt, so every warp gets the same mix of small and large primes.
 __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__restrict__ primes,
                                              const uint64_t *__restrict__ recips,
-                                             const PrimeRegions R,
+                                             const PrimeRegions R, uint32_t flags,
                                              uint64_t a, uint32_t valid, unsigned long long *prof) {
+  // diagnostics (sieve_debug_set_flags): drop whole regions (wrong results)
+  const uint32_t a1_end = flags & kFlagSkipA ? R.start : R.unit;
+  const uint32_t a2_end = flags & kFlagSkipA ? R.unit : R.cls;
+  const uint32_t b_end = flags & kFlagSkipB ? R.cls : R.warp;
+  const uint32_t c_end = flags & kFlagSkipC ? R.warp : R.big;
   const long long t0 = prof ? clock64() : 0;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t seg_end = a + 2ull * valid;
@@ -264,14 +269,14 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // unit 32 i + g goes to warp (32 i + g) mod nw, rot = 32 i mod nw
   const uint32_t c32 = 32u % nw;
   uint32_t rot = (32u * R.start) % nw;
-  for (uint32_t ib = R.start; ib < R.unit; ib += 32) {
+  for (uint32_t ib = R.start; ib < a1_end; ib += 32) {
     const uint32_t i = ib + lane;
     uint32_t pl = 0, jl = kNone;
-    if (i < R.unit) {
+    if (i < a1_end) {
       pl = __ldg(primes + i);
       jl = first_hit(a, seg_end, pl, __ldg(recips + i));
     }
-    const uint32_t nb = min(32u, R.unit - ib);
+    const uint32_t nb = min(32u, a1_end - ib);
     for (uint32_t k = 0; k < nb; ++k) {
       const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
       const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
@@ -289,10 +294,10 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
 
   // (A2) one prime per warp, lane l walks the classes l + 32 g
   // (few primes, each a lot of work: static, warp w takes primes w + nw l)
-  for (uint32_t ib = R.unit + warp; ib < R.cls; ib += 32u * nw) {
+  for (uint32_t ib = R.unit + warp; ib < a2_end; ib += 32u * nw) {
     const uint32_t i = ib + lane * nw;
     uint32_t pl = 0, jl = kNone;
-    if (i < R.cls) {
+    if (i < a2_end) {
       pl = __ldg(primes + i);
       jl = first_hit(a, seg_end, pl, __ldg(recips + i));
     }
@@ -320,10 +325,12 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // (B) one prime per warp, lane l takes the hits l + 32 s: slot j advances
   // by 32 p, i.e. its row j >> 5 by p (bank fixed), so the byte offset is
   // (4 row) & ~127 | 4 bank and the mask rotates by p.
-  for (uint32_t ib = R.cls + warp; ib < R.warp; ib += 32u * nw) {
+  const bool w32 = (valid & 31u) == 0;
+  const uint32_t Qlim32 = sb + ((valid >> 5) << 2);
+  for (uint32_t ib = R.cls + warp; ib < b_end; ib += 32u * nw) {
     const uint32_t i = ib + lane * nw;
     uint32_t pl = 0, jl = kNone;
-    if (i < R.warp) {
+    if (i < b_end) {
       pl = __ldg(primes + i);
       jl = first_hit(a, seg_end, pl, __ldg(recips + i));
     }
@@ -333,13 +340,15 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
       const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
       if (j0 == kNone) { stop = true; break; }  // and so for every later prime
       const uint32_t j = j0 + lane * p;
-      const uint32_t b4 = (j & 31u) << 2;
+      const uint32_t row = j >> 5;
+      const uint32_t b4 = (j << 2) & 124u;  // 4 bank
       // Q = shared byte address of the hit's block plus 4 (row & 31): the
       // 128-byte aligned base keeps (Q & ~127) | b4 the hit's word
-      uint32_t Q = sb + ((j >> 5) << 2);
-      uint32_t mask = t_mask(j);
-      // slot < valid <=> row < ceil((valid - bank) / 32) (0 when bank >= valid)
-      const uint32_t Qlim = sb + (((valid + 31u - (j & 31u)) >> 5) << 2);
+      uint32_t Q = sb + 4u * row;
+      uint32_t mask = __funnelshift_l(0u, 1u, row);
+      // slot < valid <=> row < ceil((valid - bank) / 32) (0 when bank >= valid);
+      // valid a multiple of 32: row < valid / 32 for every bank
+      const uint32_t Qlim = w32 ? Qlim32 : sb + (((valid + 31u - (j & 31u)) >> 5) << 2);
       const uint32_t s4 = 4u * p;
       for (; Q + 3u * s4 < Qlim; Q += 4u * s4) {
         red_or((Q & ~127u) | b4, mask);
@@ -370,19 +379,19 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // of slot j is (J >> 5) & ~127 | J & 127 and its bit is (J >> 7) & 31 (the
   // base term is a multiple of 4096, invisible to both).
   const uint32_t Jlim = 4u * valid + 32u * sb;
-  for (uint32_t k0 = R.warp + threadIdx.x; k0 < R.big; k0 += kLargeILP * blockDim.x) {
+  for (uint32_t k0 = R.warp + threadIdx.x; k0 < c_end; k0 += kLargeILP * blockDim.x) {
     uint32_t pk[kLargeILP], jk[kLargeILP];
     uint64_t rk[kLargeILP];
 #pragma unroll
     for (int u = 0; u < kLargeILP; ++u) {
-      const uint32_t k = min(k0 + u * blockDim.x, R.big - 1u);
+      const uint32_t k = min(k0 + u * blockDim.x, c_end - 1u);
       pk[u] = __ldg(primes + k);
       rk[u] = __ldg(recips + k);
     }
 #pragma unroll
     for (int u = 0; u < kLargeILP; ++u) {
       jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
-      if (k0 + u * blockDim.x >= R.big) jk[u] = kNone;
+      if (k0 + u * blockDim.x >= c_end) jk[u] = kNone;
     }
     if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
 #pragma unroll
@@ -746,7 +755,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     wheel_init<NG>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
-    if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, sR, a, valid, P.prof);
+    if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, sR, P.flags, a, valid, P.prof);
     if (buckets) {
       bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s), valid);
       bq = bq + 1u == P.ring ? 0u : bq + 1u;

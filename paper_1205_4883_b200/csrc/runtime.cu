@@ -691,7 +691,8 @@ uint64_t sieve_kernel_launches(void) { return g_launches.load(); }
 
 int sieve_debug_set_flags(uint32_t flags) {
   std::lock_guard<std::mutex> lk(g.mu);
-  if (flags & ~sv::kFlagSkipMarking) return fail(SIEVE_EINVAL, "unknown debug flags %u", flags);
+  if (flags & ~(sv::kFlagSkipMarking | sv::kFlagSkipA | sv::kFlagSkipB | sv::kFlagSkipC))
+    return fail(SIEVE_EINVAL, "unknown debug flags %u", flags);
   g.flags = flags;
   return 0;
 }
