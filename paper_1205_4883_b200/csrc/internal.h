@@ -123,7 +123,6 @@ struct SieveParams {
   uint64_t out_words;      // words of out
   uint32_t out_vec4;       // out is 16-byte aligned
   uint32_t add_two;        // 2 in [lo, hi): add (1, 2) to the result
-  uint32_t *seg_counts;    // optional per-segment prime counts (odd primes)
   uint64_t *partials;      // [2 * gridDim.x]
   unsigned int *done;      // last-block-done ticket (self-resetting)
   uint64_t *result;        // [2] count, sum mod 2^64 (batch: [2 * nintervals])
@@ -138,6 +137,13 @@ struct SieveParams {
   uint32_t ring;     // ring size R (<= kMaxRing): a hit lands at most R-1 segments ahead
   uint32_t capw;     // capacity of one bucket (>= bucket primes / warps, rounded up)
   uint32_t inv_seg;  // ceil(2^32 / seg_bits): o / S by a multiply-high and one correction
+  // list mode (step A8): the primes go straight from the segment to the list;
+  // a segment's place comes from a decoupled look-back over the segments
+  // before it (per-segment flags, tagged with the launch's epoch)
+  uint64_t *list;       // ascending u64 primes, list[0] = 2 when 2 is in range
+  uint64_t list_cap;    // entries list may hold (later primes are counted, not written)
+  unsigned long long *lflags;  // [nseg]
+  uint32_t lepoch;
 };
 
 // Diagnostic flag: skip step A4/A5 (wheel init + count/write-back only), to
@@ -148,7 +154,7 @@ constexpr uint32_t kFlagSkipMarking = 1u;
 // of each region in context.  Wrong results by design.
 constexpr uint32_t kFlagSkipA = 2u, kFlagSkipB = 4u, kFlagSkipC = 8u;
 
-enum Mode { kCount = 0, kBitmap = 1, kBatch = 2 };
+enum Mode { kCount = 0, kBitmap = 1, kBatch = 2, kList = 3 };
 
 // launchers (kernels.cu)
 cudaError_t launch_sieve(int ng, int mode, const SieveParams &p, int grid, int threads,
@@ -160,11 +166,6 @@ cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64
 uint32_t base_slices(uint32_t r);  // look-back flags the base-prime kernel needs
 cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
                            uint32_t cap, cudaStream_t s);
-cudaError_t launch_scan_segments(const uint32_t *seg_counts, uint64_t nseg, uint64_t *seg_off,
-                                 uint32_t add_two, cudaStream_t s);
-cudaError_t launch_compact(const uint32_t *bitmap, uint64_t nbits, uint64_t o0, uint32_t seg_bits,
-                           uint64_t nseg, const uint64_t *seg_off, uint32_t add_two,
-                           uint64_t *out, uint64_t cap, cudaStream_t s);
 int sieve_max_ctas_per_sm(int ng, int mode, int threads, size_t smem);
 
 }  // namespace sv

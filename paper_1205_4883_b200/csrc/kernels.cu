@@ -633,6 +633,83 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
   sum += (unsigned long long)C * a + 2ull * J;
 }
 
+constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;  // look-back flag states (A2 K1, A8 list)
+
+// A8 (list mode): the primes of one segment (natural layout, after
+// untranspose) written to the list in order.  Warp w owns a contiguous range
+// of the segment's words; pass 1 counts its primes; thread 0 publishes the
+// segment's count, finds the segment's place in the list by a decoupled
+// look-back over the earlier segments, and publishes its inclusive prefix;
+// pass 2 has the lanes of a warp take 32 consecutive words at a time, place
+// them by a warp scan of their popcounts, and write their primes.  Returns
+// the segment's count in thread 0 (0 elsewhere).
+__device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, uint64_t a,
+                                              uint32_t valid, const SieveParams &P, uint32_t *s_wc,
+                                              unsigned long long *s_off) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t nwords = (valid + 31u) >> 5;
+  const uint32_t wb = warp * nwords / nw, we = (warp + 1u) * nwords / nw;
+  uint32_t c = 0;
+  for (uint32_t w = wb + lane; w < we; w += 32u) c += __popc(~seg[w]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) s_wc[warp] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (uint32_t k = 0; k < nw; ++k) {
+      const uint32_t x = s_wc[k];
+      s_wc[k] = t;  // exclusive warp offsets
+      t += x;
+    }
+    s_wc[32] = t;
+    volatile unsigned long long *fl = P.lflags;
+    const unsigned long long tag = (unsigned long long)P.lepoch << 48;
+    unsigned long long pre = 0;  // the list offset of this segment's first prime
+    if (s == 0) {
+      pre = P.add_two ? 1ull : 0ull;  // list[0] = 2
+      fl[0] = tag | ((pre + t) << 2) | kFlagIncl;
+    } else {
+      fl[s] = tag | ((unsigned long long)t << 2) | kFlagAgg;
+      for (uint64_t j = s; j-- > 0;) {
+        unsigned long long f;
+        do { f = fl[j]; } while ((f >> 48) != P.lepoch);  // not yet published in this launch
+        pre += (f >> 2) & ((1ull << 46) - 1);
+        if ((f & 3u) == kFlagIncl) break;
+      }
+      __threadfence();
+      fl[s] = tag | ((pre + t) << 2) | kFlagIncl;
+    }
+    *s_off = pre;
+    if (s == 0 && P.add_two && P.list_cap > 0) P.list[0] = 2;
+  }
+  __syncthreads();
+  unsigned long long base = *s_off + s_wc[warp];
+  for (uint32_t w0 = wb; w0 < we; w0 += 32u) {
+    const uint32_t w = w0 + lane;
+    uint32_t x = w < we ? ~seg[w] : 0u;
+    const uint32_t cx = __popc(x);
+    uint32_t incl = cx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    unsigned long long k = base + incl - cx;
+    const uint64_t v0 = a + 64ull * w;
+    while (x) {
+      const uint32_t b = __ffs(x) - 1;
+      x &= x - 1;
+      if (k < P.list_cap) P.list[k] = v0 + 2ull * b;
+      ++k;
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  const uint64_t tot = s_wc[32];
+  __syncthreads();  // s_wc is reused by the next segment
+  return threadIdx.x == 0 ? tot : 0ull;  // counted once per CTA
+}
+
 // block-wide sum of two u64 values; result valid in thread 0
 __device__ __forceinline__ void block_sum2(unsigned long long &x, unsigned long long &y,
                                            unsigned long long *red) {
@@ -718,6 +795,8 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   __shared__ PrimeRegions sR;
   __shared__ uint32_t s_last;
   __shared__ uint32_t s_ub[5];
+  __shared__ uint32_t s_wc[33];            // list mode: warp counts / offsets, segment total
+  __shared__ unsigned long long s_off;     // list mode: the segment's place in the list
 
   for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
   compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
@@ -772,17 +851,10 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
         atomicAdd(reinterpret_cast<unsigned long long *>(P.result) + 2 * iv + 1, sm);
       }
       __syncthreads();
-    } else if (MODE == kBitmap && P.seg_counts) {
+    } else if (MODE == kList) {
       untranspose(seg, valid);
       __syncthreads();
-      unsigned long long c = 0, sm = 0;
-      epilogue<kBitmap>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, c, sm);
-      cnt += c;
-      sum += sm;
-      unsigned long long c2 = c, z = 0;
-      block_sum2(c2, z, red);
-      if (threadIdx.x == 0) P.seg_counts[s] = (uint32_t)c2;
-      __syncthreads();
+      cnt += list_emit(seg, s, a, valid, P, s_wc, &s_off);
     } else {
       if (MODE == kBitmap) {
         untranspose(seg, valid);
@@ -844,7 +916,6 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
 constexpr uint32_t kBaseThreads = 256;
 constexpr uint32_t kSliceBits = 32u * kBaseThreads;  // one word per thread
 constexpr uint32_t kMaxSmall = 1024;                 // odd primes <= 4096 number 563
-constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;
 
 __device__ __forceinline__ uint64_t make_flag(uint32_t epoch, uint64_t v, uint64_t st) {
   return ((uint64_t)epoch << 48) | (v << 2) | st;
@@ -975,138 +1046,6 @@ __global__ void k_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_
 }
 
 // ---------------------------------------------------------------------------
-// A8: list compaction.  seg_off[s] = exclusive prefix of seg_counts (+1 when
-// 2 is in range, which takes list slot 0).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_scan_segments(const uint32_t *seg_counts, uint64_t nseg,
-                                                        uint64_t *seg_off, uint32_t add_two) {
-  __shared__ unsigned long long s_w[32];
-  __shared__ unsigned long long s_carry;
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x >> 5;
-  if (tid == 0) s_carry = add_two;
-  __syncthreads();
-  for (uint64_t base = 0; base < nseg; base += blockDim.x) {
-    const uint64_t i = base + tid;
-    const unsigned long long v = i < nseg ? seg_counts[i] : 0ull;
-    unsigned long long incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= (uint32_t)o) incl += y;
-    }
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    unsigned long long off = s_carry + incl - v;
-    for (uint32_t w = 0; w < warp; ++w) off += s_w[w];
-    if (i < nseg) seg_off[i] = off;
-    __syncthreads();
-    if (tid == 0) {
-      unsigned long long t = 0;
-      for (uint32_t w = 0; w < nw; ++w) t += s_w[w];
-      s_carry += t;
-    }
-    __syncthreads();
-  }
-}
-
-// Pieces of kPieceWords bitmap words: every thread takes kCompactWPT
-// consecutive words, a block scan of the per-thread prime counts gives each
-// thread its place, the primes are expanded into a shared-memory staging
-// area in list order and the block copies the staging area to the list with
-// coalesced stores (consecutive threads, consecutive u64).  A piece with
-// more primes than the staging area holds (only for small integers, where
-// primes are dense) is written straight from the registers instead.
-constexpr uint32_t kCompactThreads = 1024;
-constexpr uint32_t kCompactWPT = 2;  // words per thread per piece
-constexpr uint32_t kPieceWords = kCompactThreads * kCompactWPT;
-constexpr uint32_t kStage = 8192;    // staged primes per piece (64 KiB)
-
-__global__ void __launch_bounds__(kCompactThreads) k_compact(
-    const uint32_t *__restrict__ bitmap, uint64_t nbits, uint64_t o0, uint32_t seg_bits, uint64_t nseg,
-    const uint64_t *__restrict__ seg_off, uint32_t add_two, uint64_t *__restrict__ out, uint64_t cap) {
-  extern __shared__ __align__(16) unsigned long long stage[];  // kStage
-  __shared__ uint32_t s_w[32];
-  __shared__ uint32_t s_tot;
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x >> 5;
-  if (add_two && blockIdx.x == 0 && tid == 0 && cap > 0) out[0] = 2;
-  const uint64_t words = (nbits + 31) / 32;
-  const uint32_t seg_words = seg_bits / 32;
-  for (uint64_t s = blockIdx.x; s < nseg; s += gridDim.x) {
-    uint64_t off = seg_off[s];
-    if (off >= cap) continue;  // everything here lands past the cap
-    const uint64_t wb = s * seg_words;
-    const uint64_t we = min(words, wb + seg_words);
-    for (uint64_t w0 = wb; w0 < we; w0 += kPieceWords) {
-      // this thread's words (w0 + 2 tid, w0 + 2 tid + 1), zero past the end
-      const uint64_t w = w0 + kCompactWPT * tid;
-      uint32_t x[kCompactWPT];
-      if (w + 1 < we) {
-        const uint2 v = __ldcs(reinterpret_cast<const uint2 *>(bitmap + w));  // 8-byte aligned: w even
-        x[0] = v.x;
-        x[1] = v.y;
-      } else {
-        x[0] = w < we ? __ldcs(bitmap + w) : 0u;
-        x[1] = 0u;
-      }
-      const uint32_t c = __popc(x[0]) + __popc(x[1]);
-      // block exclusive scan of c
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-      }
-      if (lane == 31) s_w[warp] = incl;
-      __syncthreads();
-      if (warp == 0) {
-        uint32_t t = lane < nw ? s_w[lane] : 0u, ti = t;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
-          if (lane >= (uint32_t)o) ti += y;
-        }
-        if (lane < nw) s_w[lane] = ti - t;  // exclusive warp offsets
-        if (lane == 31) s_tot = ti;
-      }
-      __syncthreads();
-      const uint32_t my = s_w[warp] + incl - c, tot = s_tot;
-      if (tot <= kStage) {
-        uint32_t k = my;
-#pragma unroll
-        for (uint32_t u = 0; u < kCompactWPT; ++u) {
-          uint32_t y = x[u];
-          const uint64_t base = o0 + 64ull * (w + u);
-          while (y) {
-            const uint32_t b = __ffs(y) - 1;
-            y &= y - 1;
-            stage[k++] = base + 2ull * b;
-          }
-        }
-        __syncthreads();
-        const uint64_t room = cap > off ? cap - off : (uint64_t)0;
-        const uint64_t n = (uint64_t)tot < room ? (uint64_t)tot : room;
-        for (uint32_t i = tid; i < n; i += blockDim.x) __stcs(out + off + i, stage[i]);
-      } else {
-        uint64_t k = off + my;
-#pragma unroll
-        for (uint32_t u = 0; u < kCompactWPT; ++u) {
-          uint32_t y = x[u];
-          const uint64_t base = o0 + 64ull * (w + u);
-          while (y) {
-            const uint32_t b = __ffs(y) - 1;
-            y &= y - 1;
-            if (k < cap) out[k] = base + 2ull * b;
-            ++k;
-          }
-        }
-      }
-      off += tot;
-      __syncthreads();  // stage and s_w are reused by the next piece
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 template <int NG, int MODE>
@@ -1135,6 +1074,7 @@ cudaError_t launch_sieve(int ng, int mode, const SieveParams &p, int grid, int t
     case kCount: return launch_m<kCount>(ng, p, grid, threads, smem, s);
     case kBitmap: return launch_m<kBitmap>(ng, p, grid, threads, smem, s);
     case kBatch: return launch_m<kBatch>(ng, p, grid, threads, smem, s);
+    case kList: return launch_m<kList>(ng, p, grid, threads, smem, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1144,7 +1084,8 @@ static cudaError_t set_attr_ng(size_t smem) {
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(k_sieve<NG, kCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
   if ((e = cudaFuncSetAttribute(k_sieve<NG, kBitmap>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-  return cudaFuncSetAttribute(k_sieve<NG, kBatch>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if ((e = cudaFuncSetAttribute(k_sieve<NG, kBatch>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  return cudaFuncSetAttribute(k_sieve<NG, kList>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 cudaError_t set_sieve_smem_limits(size_t smem) {
@@ -1155,9 +1096,6 @@ cudaError_t set_sieve_smem_limits(size_t smem) {
   if ((e = set_attr_ng<4>(smem))) return e;
   if ((e = set_attr_ng<5>(smem))) return e;
   if ((e = set_attr_ng<6>(smem))) return e;
-  if ((e = cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(kStage * 8))))
-    return e;
   return cudaSuccess;
 }
 
@@ -1193,22 +1131,6 @@ cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64
                            uint32_t cap, cudaStream_t s) {
   const int grid = (int)((cap + 255) / 256 < 1184 ? (cap + 255) / 256 : 1184);
   k_prepare<<<grid > 0 ? grid : 1, 256, 0, s>>>(primes, nbase, recips, cap);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_scan_segments(const uint32_t *seg_counts, uint64_t nseg, uint64_t *seg_off,
-                                 uint32_t add_two, cudaStream_t s) {
-  k_scan_segments<<<1, 1024, 0, s>>>(seg_counts, nseg, seg_off, add_two);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_compact(const uint32_t *bitmap, uint64_t nbits, uint64_t o0, uint32_t seg_bits,
-                           uint64_t nseg, const uint64_t *seg_off, uint32_t add_two, uint64_t *out,
-                           uint64_t cap, cudaStream_t s) {
-  int grid = nseg < 148 * 2 ? (int)nseg : 148 * 2;  // 2 x (64 KiB staging + 1024 threads) per SM
-  if (grid < 1) grid = 1;
-  k_compact<<<grid, kCompactThreads, kStage * 8, s>>>(bitmap, nbits, o0, seg_bits, nseg, seg_off,
-                                                     add_two, out, cap);
   return cudaGetLastError();
 }
 

@@ -119,14 +119,14 @@ struct Ctx {
   DevBuf<unsigned int> done;
   DevBuf<uint64_t> result;
   DevBuf<uint32_t> bitmap;
-  DevBuf<uint32_t> segcnt;
-  DevBuf<uint64_t> segoff;
   DevBuf<uint64_t> list;
   DevBuf<sv::BatchItem> items;
   DevBuf<uint64_t> bres;
   DevBuf<uint2> buckets;  // step A5 bucket rings
   DevBuf<uint64_t> kflags;  // K1 look-back flags (epoch-tagged, never reset)
   uint32_t epoch = 0;
+  DevBuf<unsigned long long> lflags;  // list-mode look-back flags (epoch-tagged)
+  uint32_t lepoch = 0;
   uint64_t *h_res = nullptr;  // pinned [2]
   unsigned long long *prof = nullptr;  // diagnostics: phase-cycle counters
   uint32_t flags = 0;                  // diagnostics: sv::kFlagSkipMarking
@@ -333,7 +333,9 @@ int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork) {
   const int grid = grid_for(nwork);
   TRY(g.partials.ensure(2 * (size_t)grid));
   sp.partials = g.partials.p;
-  if (mode != sv::kBatch) TRY(setup_buckets(sp, grid));
+  // not in list mode: its look-back needs the segments of a wave in flight
+  // together (round robin), a CTA's contiguous run would serialise it
+  if (mode == sv::kCount || mode == sv::kBitmap) TRY(setup_buckets(sp, grid));
   const int ng = ng_for_wheel(g.opt.wheel);
   CUDA_TRY(sv::launch_sieve(ng, mode, sp, grid, (int)g.opt.threads, sieve_smem(), g.stream()));
   g_launches += 1;
@@ -354,13 +356,12 @@ int stats_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, c
 }
 
 int bitmap_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase,
-                 uint32_t *out, uint32_t *segcnt, uint64_t *result) {
+                 uint32_t *out, uint64_t *result) {
   if (P.nbits == 0) return stats_async(P, primes, recips, nbase, result);
   sv::SieveParams sp = params_for(P, primes, recips, nbase, result);
   sp.out = out;
   sp.out_words = P.words;
   sp.out_vec4 = ((uintptr_t)out & 15u) == 0 ? 1u : 0u;
-  sp.seg_counts = segcnt;
   return run_sieve(sv::kBitmap, sp, P.nseg);
 }
 
@@ -410,7 +411,7 @@ int64_t do_bitmap(uint64_t lo, uint64_t hi, uint32_t *out) {
     TRY(g.bitmap.ensure(P.words));
     dst = g.bitmap.p;
   }
-  TRY(bitmap_async(P, g.primes.p, g.recips.p, g.nbase.p, dst, nullptr, g.result.p));
+  TRY(bitmap_async(P, g.primes.p, g.recips.p, g.nbase.p, dst, g.result.p));
   if (!dev)
     CUDA_TRY(cudaMemcpyAsync(out, dst, P.words * 4, cudaMemcpyDeviceToHost, g.stream()));
   uint64_t c = 0;
@@ -436,22 +437,32 @@ int64_t do_primes(uint64_t lo, uint64_t hi, uint64_t *out, uint64_t cap) {
     return P.two ? 1 : 0;
   }
   TRY(own_base(P.r));
-  TRY(g.bitmap.ensure(P.words + 4));
-  TRY(g.segcnt.ensure(P.nseg));
-  TRY(bitmap_async(P, g.primes.p, g.recips.p, g.nbase.p, g.bitmap.p, g.segcnt.p, g.result.p));
-  if (cap > 0) {
-    TRY(g.segoff.ensure(P.nseg));
-    CUDA_TRY(sv::launch_scan_segments(g.segcnt.p, P.nseg, g.segoff.p, P.two ? 1u : 0u, g.stream()));
-    g_launches += 1;
+  if (cap == 0) {  // size query: count mode
+    TRY(stats_async(P, g.primes.p, g.recips.p, g.nbase.p, g.result.p));
+  } else {
     const bool dev = is_device_ptr(out);
     uint64_t *dst = out;
     if (!dev) {
       TRY(g.list.ensure(cap));
       dst = g.list.p;
     }
-    CUDA_TRY(sv::launch_compact(g.bitmap.p, P.nbits, P.o0, (uint32_t)seg_bits(), P.nseg, g.segoff.p,
-                                P.two ? 1u : 0u, dst, cap, g.stream()));
-    g_launches += 1;
+    // list mode: one sieve launch writes the list (decoupled look-back)
+    if (P.nseg > g.lflags.n) {
+      TRY(g.lflags.ensure(P.nseg));
+      CUDA_TRY(cudaMemsetAsync(g.lflags.p, 0, g.lflags.n * sizeof(unsigned long long), g.stream()));
+      g.lepoch = 0;
+    }
+    g.lepoch = (g.lepoch + 1) & 0xFFFF;
+    if (g.lepoch == 0) {  // 2^16 launches: clear stale tags once
+      CUDA_TRY(cudaMemsetAsync(g.lflags.p, 0, g.lflags.n * sizeof(unsigned long long), g.stream()));
+      g.lepoch = 1;
+    }
+    sv::SieveParams sp = params_for(P, g.primes.p, g.recips.p, g.nbase.p, g.result.p);
+    sp.list = dst;
+    sp.list_cap = cap;
+    sp.lflags = g.lflags.p;
+    sp.lepoch = g.lepoch;
+    TRY(run_sieve(sv::kList, sp, P.nseg));
     uint64_t c = 0;
     TRY(fetch_result(&c, nullptr));
     if (!dev) {
@@ -597,7 +608,7 @@ int sieve_bitmap_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const u
   const Plan P = make_plan(lo, hi);
   if (P.words && !out) return fail(SIEVE_EINVAL, "NULL out");
   TRY(ensure_ready());
-  return bitmap_async(P, primes, recips, nbase, out, nullptr, result);
+  return bitmap_async(P, primes, recips, nbase, out, result);
 }
 
 int sieve_set_device(int ordinal) {
@@ -677,8 +688,8 @@ void sieve_shutdown(void) {
   cudaStreamSynchronize(g.stream());
   g.tables.release(); g.primes.release(); g.recips.release(); g.nbase.release();
   g.partials.release(); g.done.release(); g.result.release(); g.bitmap.release();
-  g.segcnt.release(); g.segoff.release(); g.list.release(); g.items.release(); g.bres.release();
-  g.buckets.release(); g.kflags.release();
+  g.list.release(); g.items.release(); g.bres.release();
+  g.buckets.release(); g.kflags.release(); g.lflags.release();
   if (g.h_res) cudaFreeHost(g.h_res);
   g.h_res = nullptr;
   if (g.own) cudaStreamDestroy(g.own);
