@@ -539,18 +539,29 @@ __device__ __forceinline__ void bucket_drain(const SieveParams &P, uint32_t &cnt
 // In-place 32x32 bit transpose of every 1024-slot block of the segment
 // (transposed layout -> natural layout: word w holds slots 32 w .. 32 w + 31,
 // LSB first), one block per warp at a time.  Lane r holds row r; stage w
-// swaps the off-diagonal w x w sub-blocks of every 2w x 2w block.
+// swaps the off-diagonal w x w sub-blocks of every 2w x 2w block: the lane
+// below (lane & w == 0) needs its partner's columns c - w, the lane above
+// its partner's columns c + w, so each lane sends itself rotated right by w
+// (upper partner) or 32 - w (lower partner) and merges with one bit-select:
+// three instructions (SHF, SHFL, LOP3) per stage.
 __device__ __forceinline__ void untranspose(uint32_t *seg, uint32_t valid) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t nblk = (valid + 1023u) >> 10;
+  uint32_t amt[5], keep[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const uint32_t w = 16u >> k;
+    const uint32_t m = k == 0 ? 0x0000FFFFu : k == 1 ? 0x00FF00FFu : k == 2 ? 0x0F0F0F0Fu
+                     : k == 3 ? 0x33333333u : 0x55555555u;  // columns c with (c & w) == 0
+    amt[k] = (lane & w) ? 32u - w : w;
+    keep[k] = (lane & w) ? ~m : m;
+  }
   for (uint32_t B = warp; B < nblk; B += nw) {
     uint32_t x = seg[32u * B + lane];
 #pragma unroll
-    for (int w = 16; w >= 1; w >>= 1) {
-      const uint32_t m = w == 16 ? 0x0000FFFFu : w == 8 ? 0x00FF00FFu : w == 4 ? 0x0F0F0F0Fu
-                       : w == 2 ? 0x33333333u : 0x55555555u;  // columns c with (c & w) == 0
-      const uint32_t y = __shfl_xor_sync(0xffffffffu, x, w);
-      x = (lane & w) ? ((x & ~m) | ((y >> w) & m)) : ((x & m) | ((y << w) & ~m));
+    for (int k = 0; k < 5; ++k) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, __funnelshift_r(x, x, amt[k]), 16u >> k);
+      asm("lop3.b32 %0, %0, %1, %2, 0xE4;" : "+r"(x) : "r"(y), "r"(keep[k]));  // (x & keep) | (y & ~keep)
     }
     seg[32u * B + lane] = x;
   }
