@@ -69,6 +69,7 @@ struct Plan {           // step A1 for one range [lo, hi)
   uint64_t nseg = 0;    // ceil(B/S)
   uint64_t r = 0;       // isqrt(hi-1)
   bool two = false;     // 2 in [lo, hi)
+  uint64_t sbits = 0;   // segment size S (odd slots) of this call
 };
 
 template <typename T>
@@ -214,6 +215,7 @@ int ensure_smem_attr() {
 }
 
 int grid_for(uint64_t nseg) {
+  if (g.nsm <= 0) return 148;  // before the device is initialised (planning only)
   int per = g.opt.ctas_per_sm;
   if (per <= 0) {
     per = sv::sieve_max_ctas_per_sm(0, 0, (int)g.opt.threads, sieve_smem());
@@ -231,6 +233,23 @@ int validate(uint64_t lo, uint64_t hi) {
   return 0;
 }
 
+int grid_for(uint64_t nseg);
+
+// Step A1 segment size: the range is cut into w waves of G segments (G the
+// persistent grid), w = ceil(B / (S_max G)), with S = ceil(B / (w G)) rounded
+// up to 8 KiB of slots: every CTA sieves the same number of equal segments
+// (a 2.48-wave launch would otherwise run 3 waves, the last half empty), and
+// a small range still spreads over all SMs.  S <= S_max (option segment_kb).
+uint64_t balanced_sbits(uint64_t nbits) {
+  const uint64_t smax = seg_bits();
+  if (nbits == 0) return smax;
+  const uint64_t G = (uint64_t)grid_for(~0ull);
+  const uint64_t waves = (nbits + smax * G - 1) / (smax * G);
+  uint64_t S = (nbits + waves * G - 1) / (waves * G);
+  S = (S + 65535) / 65536 * 65536;
+  return std::min(smax, std::max<uint64_t>(S, 65536));
+}
+
 Plan make_plan(uint64_t lo, uint64_t hi) {
   Plan P;
   P.lo = lo;
@@ -238,7 +257,8 @@ Plan make_plan(uint64_t lo, uint64_t hi) {
   P.o0 = lo | 1;
   P.nbits = hi > lo ? hi / 2 - lo / 2 : 0;
   P.words = (P.nbits + 31) / 32;
-  P.nseg = (P.nbits + seg_bits() - 1) / seg_bits();
+  P.sbits = balanced_sbits(P.nbits);
+  P.nseg = (P.nbits + P.sbits - 1) / P.sbits;
   P.r = hi >= 2 ? isqrt_u64(hi - 1) : 0;
   P.two = lo <= 2 && 2 < hi;
   return P;
@@ -291,7 +311,7 @@ sv::SieveParams params_for(const Plan &P, const uint32_t *primes, const uint64_t
   sp.o0 = P.o0;
   sp.nbits = P.nbits;
   sp.nseg = P.nseg;
-  sp.seg_bits = (uint32_t)seg_bits();
+  sp.seg_bits = (uint32_t)P.sbits;
   sp.r = (uint32_t)P.r;
   sp.primes = primes;
   sp.recips = recips;
