@@ -4,8 +4,9 @@ configs[2], "config 3"), count + prime sum, on 1/2/4/8 B200 (one process per
 GPU under torchrun, NCCL over NVLink for the broadcast and the all-reduce).
 
 One step = one pass of the whole hot path:
-  A2 base primes (K1, rank 0) -> A9 NCCL broadcast (N>1) -> A3-A6 segmented
-  sieve of the rank's block (count + sum) -> A9 NCCL all-reduce (N>1).
+  A2 base primes (K1; every rank, or rank 0 + A9 NCCL broadcast with
+  --broadcast) -> A3-A6 segmented sieve of the rank's block (count + sum) ->
+  A9 NCCL all-reduce (N>1).
 
 Timing: W untimed warm-up steps; then K steps bracketed by barrier +
 synchronize on both sides; every step is timed with CUDA events on the
@@ -50,8 +51,9 @@ def parse():
     ap.add_argument("--wheel", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
-    ap.add_argument("--no-broadcast", action="store_true",
-                    help="every rank recomputes the base primes instead of the NCCL broadcast")
+    ap.add_argument("--broadcast", action="store_true",
+                    help="rank 0 computes the base primes and NCCL-broadcasts them (default: every "
+                         "rank recomputes them, 18 us for config 3 -- no collective on the path)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=4 * 10**9,
                     help="integers of config 3 the oracle sieves for cpu_baseline")
@@ -238,7 +240,7 @@ def main():
     result = torch.zeros(2, dtype=torch.int64, device=dev)
     a, b = D.block_of(lo, hi, rank, world)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    bcast = world > 1 and not args.no_broadcast
+    bcast = world > 1 and args.broadcast
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
 
@@ -301,11 +303,11 @@ def main():
         verified = verified and (c, s) == (PI_1E10, SUM_1E10)
     else:
         for _ in range(2):
-            D.stats(lo, hi)
+            D.stats(lo, hi, broadcast=bcast)
         tdist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            c, s = D.stats(lo, hi)
+            c, s = D.stats(lo, hi, broadcast=bcast)
         tdist.barrier()
         e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         tdist.all_reduce(e2e_t, op=tdist.ReduceOp.MAX)
