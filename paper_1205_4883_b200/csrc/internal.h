@@ -66,6 +66,10 @@ constexpr uint32_t kUnitHits = SIEVE_UNIT_HITS;
 #define SIEVE_CLASS_HITS 16384
 #endif
 constexpr uint32_t kClassHits = SIEVE_CLASS_HITS;
+#ifndef SIEVE_A2_PARTS
+#define SIEVE_A2_PARTS 8
+#endif
+constexpr uint32_t kA2Parts = SIEVE_A2_PARTS;  // pieces per (A2) prime (divides 32)
 #ifndef SIEVE_WARP_HITS
 #define SIEVE_WARP_HITS 256
 #endif
@@ -127,7 +131,7 @@ struct SieveParams {
   unsigned int *done;      // last-block-done ticket (self-resetting)
   uint64_t *result;        // [2] count, sum mod 2^64 (batch: [2 * nintervals])
   const BatchItem *items;  // batch mode
-  unsigned long long *prof;  // optional phase-cycle counters (diagnostics), [8]
+  unsigned long long *prof;  // optional phase-cycle counters (diagnostics), [104]
   uint32_t flags;            // diagnostics: kFlagSkipMarking
   // step A5 buckets (nullptr: off).  CTA c sieves the contiguous segments
   // [c nseg / grid, (c+1) nseg / grid); bucket (c, slot, warp) holds capw

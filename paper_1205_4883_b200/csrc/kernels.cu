@@ -249,8 +249,8 @@ __device__ __forceinline__ uint32_t class_limit(uint32_t j, uint32_t valid) {
 // Every atomic of (A1)-(B) is conflict-free; (C) has random banks.  First
 // hits come from a Barrett reduction, 32 primes per warp at a time, with
 // shuffle broadcast; p^2 >= segment end stops a warp.  Work is dealt
-// statically: (A2) and (B) prime i to warp i mod nw, (C) prime i to thread
-// i mod nt, so every warp gets the same mix of small and large primes.
+// statically and evenly: (A2) in pieces round robin, (B) and (C) in
+// boustrophedon order over the warps / threads.
 __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__restrict__ primes,
                                              const uint64_t *__restrict__ recips,
                                              const PrimeRegions R, uint32_t flags,
@@ -292,33 +292,30 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   }
   const long long t1 = prof ? clock64() : 0;
 
-  // (A2) one prime per warp, lane l walks the classes l + 32 g
-  // (few primes, each a lot of work: static, warp w takes primes w + nw l)
-  for (uint32_t ib = R.unit + warp; ib < a2_end; ib += 32u * nw) {
-    const uint32_t i = ib + lane * nw;
-    uint32_t pl = 0, jl = kNone;
-    if (i < a2_end) {
-      pl = __ldg(primes + i);
-      jl = first_hit(a, seg_end, pl, __ldg(recips + i));
-    }
-    bool stop = false;
-    for (uint32_t k = 0; k < 32u; ++k) {
-      const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
-      const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
-      if (j0 == kNone) { stop = true; break; }  // and so for every later prime
-      uint32_t j = j0 + lane * p;  // first hit of class `lane`
+  // (A2) lane l walks the classes l + 32 g of one prime; the 32 class
+  // groups of a prime are cut into kA2Parts pieces dealt round robin over the
+  // warps (few primes, each a lot of work: whole primes per warp would load
+  // a dozen warps with most of the phase)
+  {
+    const uint32_t nitems = (a2_end - R.unit) * kA2Parts;
+    for (uint32_t q = warp; q < nitems; q += nw) {
+      const uint32_t i = R.unit + q / kA2Parts, h = q % kA2Parts;
+      const uint32_t p = __ldg(primes + i);
+      const uint32_t j0 = first_hit(a, seg_end, p, __ldg(recips + i));
+      if (j0 == kNone) break;  // p^2 past the segment: so for every later item of this warp
+      const uint32_t g0 = h * (32u / kA2Parts), g1 = g0 + 32u / kA2Parts;
+      uint32_t j = j0 + (lane + 32u * g0) * p;  // first hit of class lane + 32 g0
       uint32_t mask = t_mask(j);
       const uint32_t step = 128u * p, dj = 32u * p;
       if (whole) {
         const uint32_t alim = sb + ((j & 31u) << 2) + ((valid >> 10) << 7);
-        for (uint32_t g = 0; g < 32u; ++g, j += dj, mask = rotl(mask, p))
+        for (uint32_t g = g0; g < g1; ++g, j += dj, mask = rotl(mask, p))
           mark_run(sb + t_addr(j), alim, step, mask);
       } else {
-        for (uint32_t g = 0; g < 32u; ++g, j += dj, mask = rotl(mask, p))
+        for (uint32_t g = g0; g < g1; ++g, j += dj, mask = rotl(mask, p))
           mark_run(sb + t_addr(j), sb + class_limit(j, valid), step, mask);
       }
     }
-    if (stop) break;
   }
   const long long t2 = prof ? clock64() : 0;
 
@@ -327,8 +324,10 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // (4 row) & ~127 | 4 bank and the mask rotates by p.
   const bool w32 = (valid & 31u) == 0;
   const uint32_t Qlim32 = sb + ((valid >> 5) << 2);
-  for (uint32_t ib = R.cls + warp; ib < b_end; ib += 32u * nw) {
-    const uint32_t i = ib + lane * nw;
+  // prime nw m + (m even ? w : nw - 1 - w) to warp w (boustrophedon: the
+  // primes grow with the index, so a plain i mod nw loads the low warps)
+  for (uint32_t ib = R.cls; ib < b_end; ib += 32u * nw) {
+    const uint32_t i = ib + lane * nw + ((lane & 1u) ? nw - 1u - warp : warp);
     uint32_t pl = 0, jl = kNone;
     if (i < b_end) {
       pl = __ldg(primes + i);
@@ -379,19 +378,22 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // of slot j is (J >> 5) & ~127 | J & 127 and its bit is (J >> 7) & 31 (the
   // base term is a multiple of 4096, invisible to both).
   const uint32_t Jlim = 4u * valid + 32u * sb;
-  for (uint32_t k0 = R.warp + threadIdx.x; k0 < c_end; k0 += kLargeILP * blockDim.x) {
+  // round m of nt primes: thread t takes prime m nt + (m even ? t : nt - 1 - t)
+  for (uint32_t k0 = R.warp; k0 < c_end; k0 += kLargeILP * blockDim.x) {
     uint32_t pk[kLargeILP], jk[kLargeILP];
     uint64_t rk[kLargeILP];
 #pragma unroll
     for (int u = 0; u < kLargeILP; ++u) {
-      const uint32_t k = min(k0 + u * blockDim.x, c_end - 1u);
+      const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+      const uint32_t k = min(ku, c_end - 1u);
       pk[u] = __ldg(primes + k);
       rk[u] = __ldg(recips + k);
     }
 #pragma unroll
     for (int u = 0; u < kLargeILP; ++u) {
       jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
-      if (k0 + u * blockDim.x >= c_end) jk[u] = kNone;
+      const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+      if (ku >= c_end) jk[u] = kNone;
     }
     if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
 #pragma unroll
@@ -415,6 +417,10 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
       atomicAdd(prof + 4, (unsigned long long)(t2 - t1));
       atomicAdd(prof + 5, (unsigned long long)(t3 - t2));
       atomicAdd(prof + 7, (unsigned long long)(t4 - t3));
+      const uint32_t w = (threadIdx.x >> 5) & 31u;  // per-warp region cycles (load balance)
+      atomicAdd(prof + 8 + w, (unsigned long long)(t2 - t0));
+      atomicAdd(prof + 40 + w, (unsigned long long)(t3 - t2));
+      atomicAdd(prof + 72 + w, (unsigned long long)(t4 - t3));
     }
   }
 }
