@@ -110,7 +110,7 @@ struct BatchItem {
   uint32_t valid;     // odd slots in the segment (<= segment bits)
   uint32_t interval;  // index of the interval (result slot)
   uint32_t r;         // isqrt(hi_interval - 1): marking primes p <= r
-  uint32_t pad;
+  uint32_t nend;      // index of the first base prime > r (k_item_ends)
 };
 
 struct SieveParams {
@@ -170,6 +170,8 @@ cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64
 uint32_t base_slices(uint32_t r);  // look-back flags the base-prime kernel needs
 cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
                            uint32_t cap, cudaStream_t s);
+cudaError_t launch_item_ends(BatchItem *items, uint64_t n, const uint32_t *primes,
+                             const uint32_t *nbase, cudaStream_t s);
 int sieve_max_ctas_per_sm(int ng, int mode, int threads, size_t smem);
 
 }  // namespace sv

@@ -836,10 +836,18 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   for (uint64_t s = s_begin; s < s_end; s += s_step) {
     uint64_t a, bit0, o0;
     uint32_t valid;
+    PrimeRegions Ri = sR;
     if (MODE == kBatch) {
       const BatchItem it = P.items[s];
       a = it.a; valid = it.valid; o0 = it.a; bit0 = 0;
-      compute_regions(P, it.r, sR, s_ub, wheel_nprimes(NG), true);
+      // the item's primes are the prefix < it.nend (k_item_ends): clamp the
+      // regions, no search and no barrier per item
+      Ri.end = min(Ri.end, it.nend);
+      Ri.start = min(Ri.start, Ri.end);
+      Ri.unit = min(Ri.unit, Ri.end);
+      Ri.cls = min(Ri.cls, Ri.end);
+      Ri.warp = min(Ri.warp, Ri.end);
+      Ri.big = min(Ri.big, Ri.end);
     } else {
       o0 = P.o0;
       bit0 = s * (uint64_t)P.seg_bits;
@@ -851,7 +859,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     wheel_init<NG>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
-    if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, sR, P.flags, a, valid, P.prof);
+    if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof);
     if (buckets) {
       bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s), valid);
       bq = bq + 1u == P.ring ? 0u : bq + 1u;
@@ -1062,6 +1070,15 @@ __global__ void k_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_
     recips[i] = recip_of(primes[i]);
 }
 
+// A10: the prime prefix of every batch item (first index with p > r_item)
+__global__ void k_item_ends(BatchItem *items, uint64_t n, const uint32_t *__restrict__ primes,
+                            const uint32_t *__restrict__ nbase) {
+  const uint32_t nb = *nbase;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    items[i].nend = upper_bound_u32(primes, nb, items[i].r);
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -1148,6 +1165,13 @@ cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64
                            uint32_t cap, cudaStream_t s) {
   const int grid = (int)((cap + 255) / 256 < 1184 ? (cap + 255) / 256 : 1184);
   k_prepare<<<grid > 0 ? grid : 1, 256, 0, s>>>(primes, nbase, recips, cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_item_ends(BatchItem *items, uint64_t n, const uint32_t *primes,
+                             const uint32_t *nbase, cudaStream_t s) {
+  const uint64_t blocks = (n + 255) / 256;
+  k_item_ends<<<(int)(blocks < 1184 ? (blocks ? blocks : 1) : 1184), 256, 0, s>>>(items, n, primes, nbase);
   return cudaGetLastError();
 }
 

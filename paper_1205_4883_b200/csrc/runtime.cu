@@ -112,6 +112,8 @@ struct Ctx {
   bool user_set = false;
   sieve_options opt{};
   size_t smem_limit_set = 0;
+  size_t occ_key = 0;  // (shared memory, threads) of the cached occupancy
+  int occ = 0;
   DevBuf<uint32_t> tables;
   DevBuf<uint32_t> primes;
   DevBuf<uint64_t> recips;
@@ -217,9 +219,13 @@ int ensure_smem_attr() {
 int grid_for(uint64_t nseg) {
   if (g.nsm <= 0) return 148;  // before the device is initialised (planning only)
   int per = g.opt.ctas_per_sm;
-  if (per <= 0) {
-    per = sv::sieve_max_ctas_per_sm(0, 0, (int)g.opt.threads, sieve_smem());
-    if (per <= 0) per = 1;
+  if (per <= 0) {  // occupancy query cached per (threads, shared-memory size)
+    const size_t key = sieve_smem() * 2048 + g.opt.threads;
+    if (g.occ_key != key) {
+      g.occ = sv::sieve_max_ctas_per_sm(0, 0, (int)g.opt.threads, sieve_smem());
+      g.occ_key = key;
+    }
+    per = g.occ > 0 ? g.occ : 1;
   }
   uint64_t grid = (uint64_t)g.nsm * per;
   if (grid > nseg) grid = nseg;
@@ -506,20 +512,37 @@ int do_batch(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t *count
     maxhi = std::max(maxhi, hi[i]);
   }
   TRY(ensure_ready());
-  // step A10 plan: one item per (interval, segment)
+  // step A10 plan: an interval of B odd slots becomes ceil(B / S) items of
+  // equal size (one segment each), and the items are dealt largest first
+  // (their cost: the slots plus one first-hit reduction per base prime <= r)
   const uint64_t S = seg_bits();
   std::vector<sv::BatchItem> items;
+  std::vector<double> cost;
   for (uint64_t i = 0; i < n; ++i) {
     const Plan P = make_plan(lo[i], hi[i]);
-    for (uint64_t b = 0; b < P.nbits; b += S) {
+    if (P.nbits == 0) continue;
+    const uint64_t k = (P.nbits + S - 1) / S, q = P.nbits / k, rem = P.nbits % k;
+    const double np = P.r > 2 ? (double)P.r / std::log((double)P.r) : 1.0;
+    uint64_t b = 0;
+    for (uint64_t t = 0; t < k; ++t) {
       sv::BatchItem it;
       it.a = P.o0 + 2 * b;
-      it.valid = (uint32_t)std::min<uint64_t>(S, P.nbits - b);
+      it.valid = (uint32_t)(q + (t < rem ? 1 : 0));
       it.interval = (uint32_t)i;
       it.r = (uint32_t)P.r;
-      it.pad = 0;
+      it.nend = 0;
+      b += it.valid;
       items.push_back(it);
+      cost.push_back(0.6 * it.valid + 20.0 * np);
     }
+  }
+  {
+    std::vector<uint32_t> ord(items.size());
+    for (uint32_t t = 0; t < ord.size(); ++t) ord[t] = t;
+    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) { return cost[x] > cost[y]; });
+    std::vector<sv::BatchItem> sorted(items.size());
+    for (uint32_t t = 0; t < ord.size(); ++t) sorted[t] = items[ord[t]];
+    items.swap(sorted);
   }
   const uint64_t rmax = maxhi >= 2 ? isqrt_u64(maxhi - 1) : 0;
   TRY(own_base(rmax));
@@ -529,6 +552,8 @@ int do_batch(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t *count
     TRY(g.items.ensure(items.size()));
     CUDA_TRY(cudaMemcpyAsync(g.items.p, items.data(), items.size() * sizeof(sv::BatchItem),
                              cudaMemcpyHostToDevice, g.stream()));
+    CUDA_TRY(sv::launch_item_ends(g.items.p, items.size(), g.primes.p, g.nbase.p, g.stream()));
+    g_launches += 1;
     Plan dummy = make_plan(0, 0);
     sv::SieveParams sp = params_for(dummy, g.primes.p, g.recips.p, g.nbase.p, g.bres.p);
     sp.items = g.items.p;
@@ -715,6 +740,7 @@ void sieve_shutdown(void) {
   if (g.own) cudaStreamDestroy(g.own);
   g.own = nullptr;
   g.smem_limit_set = 0;
+  g.occ_key = 0;
   g.ready = false;
 }
 
