@@ -35,8 +35,8 @@ def line_of(pat, start=0):
 ms = line_of(r"^__device__ __forceinline__ void mark_segment")
 regions = [
     ("wheel", line_of(r"^struct WheelGroup"), line_of(r"^struct PrimeRegions")),
-    ("A1", line_of(r"// \(A1\) units", ms), line_of(r"// \(A2\) one prime per warp", ms)),
-    ("A2", line_of(r"// \(A2\) one prime per warp", ms), line_of(r"// \(B\) one prime per warp", ms)),
+    ("A1", line_of(r"// \(A1\) units", ms), line_of(r"// \(A2\) ", ms)),
+    ("A2", line_of(r"// \(A2\) ", ms), line_of(r"// \(B\) one prime per warp", ms)),
     ("B", line_of(r"// \(B\) one prime per warp", ms), line_of(r"// \(C\) large primes", ms)),
     ("C", line_of(r"// \(C\) large primes", ms), line_of(r"^// In-place 32x32|^// -+\n// A5|^__device__ __forceinline__ uint2 \*bucket_at", ms)),
     ("bucket", line_of(r"^__device__ __forceinline__ uint2 \*bucket_at"), line_of(r"^// In-place 32x32")),
