@@ -3,7 +3,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 PKG := paper_1205_4883_b200
-SRC := $(PKG)/csrc/kernels.cu $(PKG)/csrc/runtime.cu
+SRC := $(PKG)/csrc/kernels.cu $(PKG)/csrc/primality.cu $(PKG)/csrc/runtime.cu
 HDR := $(PKG)/csrc/internal.h include/sieve.h
 
 all: $(PKG)/libsieve.so oracle/liboracle.so
@@ -11,8 +11,8 @@ all: $(PKG)/libsieve.so oracle/liboracle.so
 $(PKG)/libsieve.so: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -shared $(SRC) -o $@ 2> build/ptxas.log || (cat build/ptxas.log; false)
 
-oracle/liboracle.so: oracle/oracle.c
-	gcc -O2 -std=c11 -shared -fPIC -pthread $< -o $@
+oracle/liboracle.so: oracle/oracle.c oracle/primality.c
+	gcc -O2 -std=c11 -shared -fPIC -pthread $^ -o $@
 
 build/k0_peaks: tools/k0_peaks.cu
 	$(NVCC) $(ARCH) -O3 -lineinfo -o $@ $<

@@ -164,6 +164,35 @@ int sieve_debug_set_profile(uint64_t *dev_counters);
  * isolation.  Results are WRONG while set; 0 restores. */
 int sieve_debug_set_flags(uint32_t flags);
 
+/* ---------------------------------------------------------------------- */
+/* the paper's second algorithm pair, batched on the    */
+/* GPU (one candidate per thread).  Every pointer of a call is either a    */
+/* device pointer (used in place, on the library stream) or a host pointer */
+/* (staged through library-owned device scratch); mixing returns           */
+/* SIEVE_EINVAL.  Calls are synchronous on return.                         */
+/* ---------------------------------------------------------------------- */
+
+/* Alg. 2 "modulo(a,b,c): exponentiating by squaring to (a^b) mod c"
+ * (SPEC.md mod_pow): out[i] = a[i]^b[i] mod c[i] for
+ * i < n, with the paper's loop (x = 1, y = a; while b > 0: if b & 1:
+ * x = x y mod c; y = y y mod c; b >>= 1) on exact 128-bit products.
+ * c[i] = 0 (a domain error) yields out[i] = UINT64_MAX; c[i] = 1 yields 0
+ * (SPEC.md: "result mod c").  Returns 0 or an error code. */
+int sieve_modpow(const uint64_t *a, const uint64_t *b, const uint64_t *c, uint64_t n, uint64_t *out);
+
+/* Alg. 3 "Fermat(p, iterations)" (SPEC.md fermat_test):
+ * out[i] = 1 iff p[i] passes `iterations` rounds, round t using the base
+ * a = draws[i*iterations + t] mod (p[i]-1) + 1 -- the caller supplies the
+ * random draws (Alg. 3's rand()), so verdicts are reproducible; draws holds
+ * n*iterations values.  p = 1 yields 0 (Alg. 3's guard), p = 0 (a domain
+ * error) yields 0.  iterations must be >= 1 (SIEVE_EINVAL otherwise). */
+int sieve_fermat(const uint64_t *p, uint64_t n, const uint64_t *draws, uint32_t iterations, uint8_t *out);
+
+/* Deterministic Miller-Rabin (bases 2, 3, 5, ..., 37: exact for every
+ * 64-bit n), the "improved primality test" of PAPER.md:235-237, used as an
+ * on-GPU verifier of sieve outputs: out[i] = 1 iff nums[i] is prime. */
+int sieve_is_prime(const uint64_t *nums, uint64_t n, uint8_t *out);
+
 #ifdef __cplusplus
 }
 #endif

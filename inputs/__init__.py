@@ -77,3 +77,15 @@ def random_intervals(n: int, seed: int, lo_max: int, width_max: int) -> list[tup
         w = g.next() % (width_max + 1)
         out.append((a, a + w))
     return out
+
+
+def u64_stream(n: int, seed: int) -> np.ndarray:
+    """n seeded uniform 64-bit values (splitmix64): the rand() draws of Alg. 3
+     and random operands for the F2 parity tests.  Vectorised
+    form of SplitMix64 (same sequence)."""
+    s = (np.arange(1, n + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+         + np.uint64(seed & MASK64))
+    z = s
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))

@@ -18,6 +18,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "primality.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 _u64 = ctypes.c_uint64
@@ -26,10 +27,11 @@ _p = ctypes.c_void_p
 
 def build(force: bool = False) -> str:
     """Compile oracle.c into liboracle.so (plain gcc -O2, no tuning)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f)
+                                                   for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-pthread",
-                               _SRC, "-o", tmp])
+                               *_SRCS, "-o", tmp])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -53,6 +55,14 @@ def lib():
         L.oracle_fnv1a64.restype = _u64
         L.oracle_batch.argtypes = [_p, _p, _u64, ctypes.c_int, _p, _p]
         L.oracle_batch.restype = ctypes.c_int
+        L.oracle_modpow.argtypes = [_u64, _u64, _u64]
+        L.oracle_modpow.restype = _u64
+        L.oracle_fermat.argtypes = [_u64, ctypes.c_uint32, _p]
+        L.oracle_fermat.restype = ctypes.c_int
+        L.oracle_modpow_batch.argtypes = [_p, _p, _p, _u64, _p]
+        L.oracle_modpow_batch.restype = None
+        L.oracle_fermat_batch.argtypes = [_p, _u64, _p, ctypes.c_uint32, _p]
+        L.oracle_fermat_batch.restype = None
         _lib = L
     return _lib
 
@@ -131,3 +141,34 @@ def batch(lo, hi, threads: int | None = None) -> tuple[np.ndarray, np.ndarray]:
     _check(lib().oracle_batch(lo.ctypes.data, hi.ctypes.data, n, threads or default_threads(),
                               cnt.ctypes.data, sm.ctypes.data))
     return cnt[:n], sm[:n]
+
+
+# ---- Alg. 2 and Alg. 3 (oracle/primality.c) -------------
+def modpow(a: int, b: int, c: int) -> int:
+    """Alg. 2: a^b mod c; UINT64_MAX for c = 0."""
+    return int(lib().oracle_modpow(a, b, c))
+
+
+def modpow_batch(a, b, c) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    b = np.ascontiguousarray(b, dtype=np.uint64)
+    c = np.ascontiguousarray(c, dtype=np.uint64)
+    out = np.zeros(a.size, dtype=np.uint64)
+    lib().oracle_modpow_batch(a.ctypes.data, b.ctypes.data, c.ctypes.data, a.size, out.ctypes.data)
+    return out
+
+
+def fermat(p: int, iterations: int, draws) -> bool:
+    """Alg. 3 with the caller's draws as rand()."""
+    d = np.ascontiguousarray(draws, dtype=np.uint64)
+    assert d.size >= iterations
+    return bool(lib().oracle_fermat(p, iterations, d.ctypes.data))
+
+
+def fermat_batch(p, draws, iterations: int) -> np.ndarray:
+    p = np.ascontiguousarray(p, dtype=np.uint64)
+    d = np.ascontiguousarray(draws, dtype=np.uint64)
+    assert d.size >= p.size * iterations
+    out = np.zeros(p.size, dtype=np.uint8)
+    lib().oracle_fermat_batch(p.ctypes.data, p.size, d.ctypes.data, iterations, out.ctypes.data)
+    return out

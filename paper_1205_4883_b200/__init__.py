@@ -17,11 +17,14 @@ from ._abi import (  # noqa: F401
     count,
     debug_set_flags,
     debug_set_profile,
+    fermat,
     get_options,
     get_stream,
+    is_prime,
     kernel_launches,
     lib,
     library_path,
+    modpow,
     prepare_base_async,
     primes,
     set_device,
@@ -36,5 +39,5 @@ __all__ = [
     "SieveError", "count", "bitmap", "primes", "stats", "batch", "bitmap_words",
     "base_capacity", "base_primes_async", "prepare_base_async", "stats_async", "bitmap_async",
     "set_device", "set_stream", "get_stream", "set_options", "get_options", "shutdown",
-    "kernel_launches", "lib", "library_path",
+    "kernel_launches", "lib", "library_path", "modpow", "fermat", "is_prime",
 ]

@@ -69,6 +69,9 @@ def lib():
             "sieve_kernel_launches": (_u64, []),
             "sieve_debug_set_profile": (ctypes.c_int, [_p]),
             "sieve_debug_set_flags": (ctypes.c_int, [ctypes.c_uint32]),
+            "sieve_modpow": (ctypes.c_int, [_p, _p, _p, _u64, _p]),
+            "sieve_fermat": (ctypes.c_int, [_p, _u64, _p, ctypes.c_uint32, _p]),
+            "sieve_is_prime": (ctypes.c_int, [_p, _u64, _p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -165,6 +168,44 @@ def stats_async(lo: int, hi: int, primes_t, recips_t, nbase_t, result_t) -> None
 def bitmap_async(lo: int, hi: int, primes_t, recips_t, nbase_t, out_t, result_t) -> None:
     _check(lib().sieve_bitmap_async(lo, hi, _ptr(primes_t), _ptr(recips_t), _ptr(nbase_t),
                                     _ptr(out_t), _ptr(result_t)))
+
+
+# ---- Alg. 2, Alg. 3, deterministic Miller-Rabin ----------
+def _u64arr(x):
+    if hasattr(x, "data_ptr"):
+        return x
+    return np.ascontiguousarray(x, dtype=np.uint64)
+
+
+def modpow(a, b, c, out=None):
+    """Alg. 2 batched: a^b mod c elementwise (numpy uint64 arrays or CUDA int64 tensors)."""
+    a, b, c = _u64arr(a), _u64arr(b), _u64arr(c)
+    n = int(a.numel() if hasattr(a, "numel") else a.size)
+    if out is None:
+        out = np.zeros(n, dtype=np.uint64)
+    _check(lib().sieve_modpow(_ptr(a), _ptr(b), _ptr(c), n, _ptr(out)))
+    return out
+
+
+def fermat(p, draws, iterations: int, out=None):
+    """Alg. 3 batched: verdict per candidate (1 = passes `iterations` rounds with
+    bases draws[i*iterations + t] mod (p-1) + 1)."""
+    p, draws = _u64arr(p), _u64arr(draws)
+    n = int(p.numel() if hasattr(p, "numel") else p.size)
+    if out is None:
+        out = np.zeros(n, dtype=np.uint8)
+    _check(lib().sieve_fermat(_ptr(p), n, _ptr(draws), iterations, _ptr(out)))
+    return out
+
+
+def is_prime(nums, out=None):
+    """Deterministic Miller-Rabin per 64-bit number (1 = prime)."""
+    nums = _u64arr(nums)
+    n = int(nums.numel() if hasattr(nums, "numel") else nums.size)
+    if out is None:
+        out = np.zeros(n, dtype=np.uint8)
+    _check(lib().sieve_is_prime(_ptr(nums), n, _ptr(out)))
+    return out
 
 
 # ---- configuration ----------------------------------------------------------

@@ -172,6 +172,12 @@ cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64
                            uint32_t cap, cudaStream_t s);
 cudaError_t launch_item_ends(BatchItem *items, uint64_t n, const uint32_t *primes,
                              const uint32_t *nbase, cudaStream_t s);
+// primality.cu (Alg. 2, Alg. 3, deterministic Miller-Rabin)
+cudaError_t launch_modpow(const uint64_t *a, const uint64_t *b, const uint64_t *c, uint64_t n,
+                          uint64_t *out, cudaStream_t s);
+cudaError_t launch_fermat(const uint64_t *p, uint64_t n, const uint64_t *draws, uint32_t iters,
+                          uint8_t *out, cudaStream_t s);
+cudaError_t launch_is_prime(const uint64_t *nums, uint64_t n, uint8_t *out, cudaStream_t s);
 int sieve_max_ctas_per_sm(int ng, int mode, int threads, size_t smem);
 
 }  // namespace sv

@@ -573,6 +573,66 @@ int do_batch(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t *count
   return 0;
 }
 
+// Step F2 calls: all pointers of a call on the device (used in place) or all
+// on the host (staged through device scratch).  Returns 0 or an error code.
+struct Staged {
+  DevBuf<uint8_t> buf;
+};
+Staged g_f2;
+
+int f2_run(const void *const *in, const size_t *in_bytes, int nin, void *out, size_t out_bytes,
+           int (*launch)(void *const *dev_in, void *dev_out, cudaStream_t s)) {
+  bool any_dev = false, any_host = false;
+  for (int k = 0; k < nin; ++k) (is_device_ptr(in[k]) ? any_dev : any_host) = true;
+  (is_device_ptr(out) ? any_dev : any_host) = true;
+  if (any_dev && any_host) return fail(SIEVE_EINVAL, "mixed host and device pointers");
+  if (any_dev) {
+    void *dev_in[4];
+    for (int k = 0; k < nin; ++k) dev_in[k] = const_cast<void *>(in[k]);
+    TRY(launch(dev_in, out, g.stream()));
+    CUDA_TRY(cudaStreamSynchronize(g.stream()));
+    return 0;
+  }
+  size_t total = out_bytes;
+  size_t off[4];
+  for (int k = 0; k < nin; ++k) {
+    off[k] = (total + 15) / 16 * 16;
+    total = off[k] + in_bytes[k];
+  }
+  TRY(g_f2.buf.ensure(total + 16));
+  uint8_t *base = g_f2.buf.p;
+  void *dev_in[4];
+  for (int k = 0; k < nin; ++k) {
+    dev_in[k] = base + off[k];
+    CUDA_TRY(cudaMemcpyAsync(dev_in[k], in[k], in_bytes[k], cudaMemcpyHostToDevice, g.stream()));
+  }
+  TRY(launch(dev_in, base, g.stream()));
+  CUDA_TRY(cudaMemcpyAsync(out, base, out_bytes, cudaMemcpyDeviceToHost, g.stream()));
+  CUDA_TRY(cudaStreamSynchronize(g.stream()));
+  return 0;
+}
+
+uint64_t f2_n = 0;
+uint32_t f2_iters = 0;
+
+int launch_modpow_cb(void *const *d, void *o, cudaStream_t s) {
+  CUDA_TRY(sv::launch_modpow((const uint64_t *)d[0], (const uint64_t *)d[1], (const uint64_t *)d[2],
+                             f2_n, (uint64_t *)o, s));
+  g_launches += 1;
+  return 0;
+}
+int launch_fermat_cb(void *const *d, void *o, cudaStream_t s) {
+  CUDA_TRY(sv::launch_fermat((const uint64_t *)d[0], f2_n, (const uint64_t *)d[1], f2_iters,
+                             (uint8_t *)o, s));
+  g_launches += 1;
+  return 0;
+}
+int launch_is_prime_cb(void *const *d, void *o, cudaStream_t s) {
+  CUDA_TRY(sv::launch_is_prime((const uint64_t *)d[0], f2_n, (uint8_t *)o, s));
+  g_launches += 1;
+  return 0;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -734,7 +794,7 @@ void sieve_shutdown(void) {
   g.tables.release(); g.primes.release(); g.recips.release(); g.nbase.release();
   g.partials.release(); g.done.release(); g.result.release(); g.bitmap.release();
   g.list.release(); g.items.release(); g.bres.release();
-  g.buckets.release(); g.kflags.release(); g.lflags.release();
+  g.buckets.release(); g.kflags.release(); g.lflags.release(); g_f2.buf.release();
   if (g.h_res) cudaFreeHost(g.h_res);
   g.h_res = nullptr;
   if (g.own) cudaStreamDestroy(g.own);
@@ -745,6 +805,42 @@ void sieve_shutdown(void) {
 }
 
 uint64_t sieve_kernel_launches(void) { return g_launches.load(); }
+
+int sieve_modpow(const uint64_t *a, const uint64_t *b, const uint64_t *c, uint64_t n, uint64_t *out) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (n == 0) return 0;
+  if (!a || !b || !c || !out) return fail(SIEVE_EINVAL, "NULL array in sieve_modpow");
+  TRY(ensure_ready());
+  f2_n = n;
+  const void *in[3] = {a, b, c};
+  const size_t by[3] = {n * 8, n * 8, n * 8};
+  return f2_run(in, by, 3, out, n * 8, launch_modpow_cb);
+}
+
+int sieve_fermat(const uint64_t *p, uint64_t n, const uint64_t *draws, uint32_t iterations,
+                 uint8_t *out) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (n == 0) return 0;
+  if (iterations == 0) return fail(SIEVE_EINVAL, "iterations must be >= 1 (SPEC.md fermat_test)");
+  if (!p || !draws || !out) return fail(SIEVE_EINVAL, "NULL array in sieve_fermat");
+  TRY(ensure_ready());
+  f2_n = n;
+  f2_iters = iterations;
+  const void *in[2] = {p, draws};
+  const size_t by[2] = {n * 8, n * (size_t)iterations * 8};
+  return f2_run(in, by, 2, out, n, launch_fermat_cb);
+}
+
+int sieve_is_prime(const uint64_t *nums, uint64_t n, uint8_t *out) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (n == 0) return 0;
+  if (!nums || !out) return fail(SIEVE_EINVAL, "NULL array in sieve_is_prime");
+  TRY(ensure_ready());
+  f2_n = n;
+  const void *in[1] = {nums};
+  const size_t by[1] = {n * 8};
+  return f2_run(in, by, 1, out, n, launch_is_prime_cb);
+}
 
 int sieve_debug_set_flags(uint32_t flags) {
   std::lock_guard<std::mutex> lk(g.mu);

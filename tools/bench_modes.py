@@ -11,6 +11,7 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import inputs  # noqa: E402
@@ -153,6 +154,37 @@ def config4_list(seg_kb=0):
     sv.set_options()
 
 
+def f2():
+    """SURVEY.md 8(f) F2 on the GPU: the deterministic Miller-Rabin verifier
+    and Alg. 3 (one round) over the whole config-4 prime list, device-resident
+    (361,840,208 candidates of ~40 bits)."""
+    lo, hi = inputs.CONFIG4
+    n = 361840208
+    lst = torch.empty(n, dtype=torch.int64, device=dev)
+    sv.primes(lo, hi, cap=n, out=lst)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    draws = torch.from_numpy(inputs.u64_stream(n, seed=7).view(np.int64)).to(dev)
+
+    def t(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+    mr = t(lambda: sv.is_prime(lst, out=out))
+    ok_mr = bool(out.all())
+    fe = t(lambda: sv.fermat(lst, draws, 1, out=out))
+    ok_fe = bool(out.all())
+    emit({"config": "F2", "mode": "Miller-Rabin (12 bases) + Fermat (Alg. 3, 1 round) over the config-4 list",
+          "candidates": n, "mr_ms": mr * 1e3, "mr_tests_per_s": n / mr, "mr_all_prime": ok_mr,
+          "fermat_ms": fe * 1e3, "fermat_tests_per_s": n / fe, "fermat_all_pass": ok_fe})
+    del lst, out, draws
+    torch.cuda.empty_cache()
+
+
 def config5():
     lo, hi = inputs.config5_intervals()
     total = int((hi - lo).sum())
@@ -186,3 +218,5 @@ if __name__ == "__main__":
         config4_list()
     if "5" in which:
         config5()
+    if "f2" in which:
+        f2()
