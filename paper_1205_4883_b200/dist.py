@@ -192,3 +192,112 @@ def batch(lo, hi, group=None, batch_fn=None, device=None):
         count[idx] = arr[: len(idx), 0]
         ssum[idx] = arr[: len(idx), 1]
     return count, ssum
+
+
+# ---------------------------------------------------------------- F1: gather
+# SURVEY.md 8(f) F1, the "gather" step of the paper's flow (PAPER.md:163-169
+# via SPEC.md:296: results gathered in node order): the per-GPU bitmap and
+# list slices assembled on every rank.  The blocks of block_of() start on
+# 32-bit words of the whole range's odd-only grid, so block g's bitmap is
+# exactly words [w_g, w_{g+1}) of the whole bitmap, and block g's primes
+# follow block g-1's.  NCCL all_gather wants equal sizes: slices are padded
+# to the largest and trimmed after.  A decomposable checksum of the bitmap,
+# sum_w (w+1) word_w mod 2^64 over global word indices, is all-reduced so
+# every rank can check the gathered copy without a sequential FNV.
+
+def _block_words(lo: int, hi: int, world: int) -> list[tuple[int, int]]:
+    """(first global word, word count) of every block's bitmap."""
+    o0 = lo | 1
+    out = []
+    for g in range(world):
+        a, b = block_of(lo, hi, g, world)
+        w0 = ((a | 1) - o0) // 64 if b > a else 0
+        nbits = b // 2 - a // 2 if b > a else 0
+        out.append((w0, (nbits + 31) // 32))
+    return out
+
+
+def bitmap_checksum(words: np.ndarray, first_word: int = 0) -> int:
+    """sum_w (first_word + w + 1) * words[w] mod 2^64 (host, exact)."""
+    w = np.asarray(words).astype(np.uint64)
+    idx = np.arange(first_word + 1, first_word + 1 + w.size, dtype=np.uint64)
+    return int(np.sum(idx * w, dtype=np.uint64))
+
+
+class CudaGatherBackend:
+    """The product compute path for F1: per-rank bitmap / list of a block on
+    the current device (C ABI), returned as CUDA tensors."""
+
+    def bitmap(self, a, b, device):
+        import torch
+        import paper_1205_4883_b200 as sv
+        n = sv.bitmap_words(a, b)
+        out = torch.zeros(max(n, 1), dtype=torch.int32, device=device)
+        if n:
+            sv.bitmap(a, b, out=out)
+        return out[:n]
+
+    def primes(self, a, b, device):
+        import torch
+        import paper_1205_4883_b200 as sv
+        n = sv.count(a, b)
+        out = torch.zeros(max(n, 1), dtype=torch.int64, device=device)
+        if n:
+            sv.primes(a, b, cap=n, out=out)
+        return out[:n]
+
+
+def _gather_padded(t, group, world):
+    """all_gather of 1-D tensors of different lengths (padded to the max)."""
+    import torch
+    import torch.distributed as dist
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    ns = [int(x.item()) for x in ns]
+    m = max(ns) if ns else 0
+    pad = torch.zeros(max(m, 1), dtype=t.dtype, device=t.device)
+    pad[: t.numel()] = t
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(outs, pad, group=group)
+    return torch.cat([o[:k] for o, k in zip(outs, ns)]) if world else t
+
+
+def gather_bitmap(lo: int, hi: int, group=None, backend=None, device=None):
+    """The whole odd-only bitmap of [lo, hi) (reading R5) on every rank:
+    each rank sieves its block, the slices are all-gathered in block order.
+    Returns (words as int32 tensor, checksum) where checksum is the
+    all-reduced decomposable checksum of the slices (== bitmap_checksum of
+    the gathered words)."""
+    import torch
+    import torch.distributed as dist
+    be = backend if backend is not None else CudaGatherBackend()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    a, b = block_of(lo, hi, rank, world)
+    mine = be.bitmap(a, b, dev)
+    w0 = _block_words(lo, hi, world)[rank][0]
+    part = bitmap_checksum(mine.cpu().numpy().view(np.uint32), w0)
+    cs = torch.tensor([u64_to_i64(part)], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(cs, op=dist.ReduceOp.SUM, group=group)
+        full = _gather_padded(mine, group, world)
+    else:
+        full = mine
+    return full, i64_to_u64(int(cs.item()))
+
+
+def gather_primes(lo: int, hi: int, group=None, backend=None, device=None):
+    """The whole ascending prime list of [lo, hi) on every rank: per-rank
+    block lists all-gathered in block order (block g's primes follow block
+    g-1's).  Returns an int64 tensor."""
+    import torch
+    import torch.distributed as dist
+    be = backend if backend is not None else CudaGatherBackend()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    a, b = block_of(lo, hi, rank, world)
+    mine = be.primes(a, b, dev)
+    return _gather_padded(mine, group, world) if world > 1 else mine

@@ -1,7 +1,8 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the multi-GPU host logic
 in paper_1205_4883_b200/dist.py: block partition, the packed base-prime
-broadcast, the u64-as-int64 all-reduce, and the LPT batch assignment with
-its all_gather reassembly.  The per-rank compute is injected (a CPU stand-in
+broadcast, the u64-as-int64 all-reduce, the LPT batch assignment with its
+all_gather reassembly, and the F1 gather of per-rank bitmaps and lists with
+the decomposable bitmap checksum.  The per-rank compute is injected (a CPU stand-in
 built on the oracle) because this container has no GPU; the CUDA backend is
 the default in the product path and is exercised by the -m gpu tests."""
 import os
@@ -55,6 +56,17 @@ class OracleBackend:
         result[1] = D.u64_to_i64(s)
 
 
+class OracleGatherBackend:
+    """CPU stand-in for CudaGatherBackend (test only)."""
+
+    def bitmap(self, a, b, device):
+        bm, _, _ = oracle.bitmap(a, b)
+        return torch.from_numpy(bm.view(np.int32).copy())
+
+    def primes(self, a, b, device):
+        return torch.from_numpy(oracle.primes(a, b).view(np.int64).copy())
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -73,6 +85,11 @@ def _worker(rank, world, port, q):
         t = torch.tensor([D.u64_to_i64((1 << 64) - 5 if rank == 0 else 9)], dtype=torch.int64)
         dist.all_reduce(t)
         out["wrap"] = D.i64_to_u64(int(t.item()))
+        gb = OracleGatherBackend()
+        for lo, hi in [(2, 2 * 10**5 + 1), (10**9 + 7, 10**9 + 3 * 10**5), (3, 3), (10, 12)]:
+            words, cs = D.gather_bitmap(lo, hi, backend=gb, device=cpu)
+            lst = D.gather_primes(lo, hi, backend=gb, device=cpu)
+            out[("F1", lo, hi)] = (words.numpy().view(np.uint32).tolist(), cs, lst.numpy().tolist())
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -92,7 +109,14 @@ def test_two_rank_gloo_stats_batch_and_wrap():
     assert res[0] == res[1]
     r = res[0]
     for key, val in r.items():
-        if isinstance(key, tuple):
+        if isinstance(key, tuple) and key[0] == "F1":
+            _, lo, hi = key
+            words, cs, lst = val
+            obm, _, _ = oracle.bitmap(lo, hi)
+            assert words == obm.tolist(), key                     # gathered bitmap == whole bitmap
+            assert cs == D.bitmap_checksum(obm), key              # all-reduced decomposable checksum
+            assert lst == oracle.primes(lo, hi).tolist(), key     # gathered list == whole list
+        elif isinstance(key, tuple):
             assert val == oracle.stats(*key), key
     lo5, hi5 = inputs.config5_intervals(64)
     oc, os_ = oracle.batch(lo5, hi5)

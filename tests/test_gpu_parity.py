@@ -280,3 +280,18 @@ def test_config4_full_list_on_device_subwindows():
             assert np.array_equal(sl, oracle.primes(s, s + 10**7))
     del out
     torch.cuda.empty_cache()
+
+
+def test_f1_gather_single_rank_cuda_backend():
+    """F1 on the CUDA backend at world size 1 (the box has one GPU; the
+    N-rank gather logic runs under gloo in test_dist_gloo.py): the whole
+    config-1 bitmap with its decomposable checksum, and the whole list."""
+    import torch
+    from paper_1205_4883_b200 import dist as D
+    lo, hi = inputs.CONFIG1
+    words, cs = D.gather_bitmap(lo, hi, device=torch.device("cuda"))
+    w = words.cpu().numpy().view(np.uint32)
+    assert _fnv(w) == int(PINS["config1.fnv"], 16)
+    assert cs == D.bitmap_checksum(w)
+    lst = D.gather_primes(lo, hi, device=torch.device("cuda")).cpu().numpy().view(np.uint64)
+    assert lst.size == int(PINS["config1.count"]) and int(lst.sum(dtype=np.uint64)) == int(PINS["config1.sum"])
