@@ -295,3 +295,19 @@ def test_f1_gather_single_rank_cuda_backend():
     assert cs == D.bitmap_checksum(w)
     lst = D.gather_primes(lo, hi, device=torch.device("cuda")).cpu().numpy().view(np.uint64)
     assert lst.size == int(PINS["config1.count"]) and int(lst.sum(dtype=np.uint64)) == int(PINS["config1.sum"])
+
+
+@pytest.mark.parametrize("seg_kb,buckets", [(208, 0), (16, 0), (16, 1)])
+def test_top_of_range_2_48(seg_kb, buckets):
+    """The largest allowed range end, hi = 2^48 (base primes up to 2^24,
+    ~1.08 M of them; the widest K1 launch): count, sum and the list of a
+    window just below it, against the oracle, with and without buckets."""
+    sv.set_options(segment_kb=seg_kb, buckets=buckets)
+    hi = 1 << 48
+    lo = hi - 3 * 10**6 - 17
+    assert sv.stats(lo, hi) == oracle.stats(lo, hi)
+    lst, c = sv.primes(lo, hi)
+    assert np.array_equal(lst, oracle.primes(lo, hi))
+    bm, cb = sv.bitmap(lo, hi)
+    obm, oc, _ = oracle.bitmap(lo, hi)
+    assert cb == oc and np.array_equal(bm, obm)
