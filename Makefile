@@ -3,8 +3,8 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 PKG := paper_1205_4883_b200
-SRC := $(PKG)/csrc/kernels.cu $(PKG)/csrc/primality.cu $(PKG)/csrc/runtime.cu
-HDR := $(PKG)/csrc/internal.h include/sieve.h
+SRC := $(PKG)/csrc/kernels.cu $(PKG)/csrc/primality.cu $(PKG)/csrc/peer.cu $(PKG)/csrc/runtime.cu
+HDR := $(PKG)/csrc/internal.h $(PKG)/csrc/peer.cuh include/sieve.h
 
 all: $(PKG)/libsieve.so oracle/liboracle.so
 

@@ -1,12 +1,13 @@
 #!/usr/bin/env python
 """Headline benchmark: sieved integers/s for pi(N), N = 1e10 (BASELINE.json
 configs[2], "config 3"), count + prime sum, on 1/2/4/8 B200 (one process per
-GPU under torchrun, NCCL over NVLink for the broadcast and the all-reduce).
+GPU under torchrun).
 
 One step = one pass of the whole hot path:
   A2 base primes (K1; every rank, or rank 0 + A9 NCCL broadcast with
   --broadcast) -> A3-A6 segmented sieve of the rank's block (count + sum) ->
-  A9 NCCL all-reduce (N>1).
+  A9 all-reduce (N>1): by default inside the sieve kernel's last CTA over
+  NVLink peer memory (F4, csrc/peer.cuh), `--allreduce nccl` for NCCL.
 
 Timing: W untimed warm-up steps; then K steps bracketed by barrier +
 synchronize on both sides; every step is timed with CUDA events on the
@@ -54,6 +55,10 @@ def parse():
     ap.add_argument("--broadcast", action="store_true",
                     help="rank 0 computes the base primes and NCCL-broadcasts them (default: every "
                          "rank recomputes them, 18 us for config 3 -- no collective on the path)")
+    ap.add_argument("--allreduce", choices=["fused", "nccl"], default="fused",
+                    help="N>1: the (count, sum) all-reduce inside the sieve kernel over NVLink peer "
+                         "memory (F4, csrc/peer.cuh; falls back to nccl on every rank if any rank "
+                         "cannot attach or verify it) or a separate NCCL all-reduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=4 * 10**9,
                     help="integers of config 3 the oracle sieves for cpu_baseline")
@@ -241,6 +246,23 @@ def main():
     a, b = D.block_of(lo, hi, rank, world)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
     bcast = world > 1 and args.broadcast
+    fused = world > 1 and args.allreduce == "fused"
+
+    def all_ok(ok: bool) -> bool:  # the same decision on every rank
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MIN)
+        return bool(t.item())
+
+    if fused:
+        try:
+            D.attach_peers(timeout_ms=2000)
+            ok = True
+        except Exception as ex:  # e.g. CUDA IPC unavailable in this container
+            print(f"rank {rank}: fused all-reduce unavailable ({ex})", file=sys.stderr)
+            ok = False
+        if not all_ok(ok):
+            fused = False
+            D.detach_peers()
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
 
@@ -252,9 +274,12 @@ def main():
             if bcast:
                 tdist.broadcast(base.packed, src=0)
             if e: e[1].record(stream)
-            sv.stats_async(a, b, base.primes, base.recips, base.nbase, result)
+            if fused:  # sieve + all-reduce in one kernel
+                sv.stats_allreduce_async(a, b, base.primes, base.recips, base.nbase, result)
+            else:
+                sv.stats_async(a, b, base.primes, base.recips, base.nbase, result)
             if e: e[2].record(stream)
-            if world > 1:
+            if world > 1 and not fused:
                 tdist.all_reduce(result, op=tdist.ReduceOp.SUM)
             if e: e[3].record(stream)
 
@@ -263,6 +288,15 @@ def main():
     torch.cuda.synchronize()
     got = [D.i64_to_u64(x) for x in result.cpu().tolist()]
     verified = (got[0] == PI_1E10 and got[1] == SUM_1E10)
+    if fused and not all_ok(verified):  # fall back together, re-warm
+        print(f"rank {rank}: fused all-reduce gave {got}; using NCCL", file=sys.stderr)
+        fused = False
+        D.detach_peers()
+        for _ in range(max(args.warmup, 0)):
+            step()
+        torch.cuda.synchronize()
+        got = [D.i64_to_u64(x) for x in result.cpu().tolist()]
+        verified = (got[0] == PI_1E10 and got[1] == SUM_1E10)
 
     launches0 = sv.kernel_launches()
     sampler = ClockSampler(local)
@@ -335,7 +369,10 @@ def main():
                        "lo": lo, "hi": hi, "segment_kb": opts["segment_kb"], "wheel": opts["wheel"],
                        "threads": opts["threads"], "base_primes": "broadcast" if bcast else "per-rank",
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
-                       "parallelism": f"range split over {world} GPU(s)"},
+                       "parallelism": f"range split over {world} GPU(s)",
+                       "allreduce": ("none" if world == 1 else
+                                     "fused in the sieve kernel (NVLink peer memory)" if fused
+                                     else "NCCL all_reduce")},
             "verified": verified,
             "base_ms": statistics.mean(base_ms),
             "wall_ms_per_step_incl_flush": t_wall * 1e3 / args.steps,

@@ -139,6 +139,52 @@ int sieve_bitmap_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const u
                        const uint32_t *nbase, uint32_t *out, uint64_t *result);
 
 /* ---------------------------------------------------------------------- */
+/* the gather of the paper's flow (PAPER.md:163-169,    */
+/* Fig. 6 -- every node's result collected after its sieve) for the        */
+/* count/sum path, fused into the sieve kernel: its last CTA writes this   */
+/* rank's (count, sum) into every peer's slab over NVLink (P2P stores of   */
+/* CUDA-IPC-mapped memory) and sums the slots the peers wrote into its own  */
+/* -- no separate collective launch.  One process per GPU; the calls below */
+/* are collective in the SPMD sense: every rank makes the same sequence of */
+/* sieve_stats_allreduce_async calls.                                       */
+/* ---------------------------------------------------------------------- */
+#define SIEVE_IPC_HANDLE_BYTES 64
+#define SIEVE_MAX_PEERS 64
+
+/* Allocates (once) this process's slab on its device, zeroed, and writes
+ * its cudaIpcMemHandle (SIEVE_IPC_HANDLE_BYTES bytes) into handle_out, to
+ * be exchanged with the other ranks (e.g. an all_gather over the host). */
+int sieve_peer_slab_handle(void *handle_out);
+
+/* handles: world x SIEVE_IPC_HANDLE_BYTES, rank order (this rank's own
+ * entry is ignored).  Opens every peer's slab (peer access enabled lazily),
+ * zeroes this rank's slab and resets the launch epoch.  Every rank must
+ * have attached (e.g. a barrier after this call) before the first fused
+ * launch.  timeout_ms bounds each fused launch's wait for its peers (0 =
+ * 10 s): a wait that expires yields result = {2^64-1, 2^64-1} instead of a
+ * hung GPU.  1 <= world <= SIEVE_MAX_PEERS, 0 <= rank < world. */
+int sieve_peer_attach(const void *handles, int world, int rank, uint32_t timeout_ms);
+
+/* As sieve_peer_attach with the slabs given as device pointers valid in
+ * this process (world entries, rank order; caller-owned, each >= 4 KiB;
+ * slabs[rank] zeroed by the caller before the first fused launch). */
+int sieve_peer_attach_ptrs(void *const *slabs, int world, int rank, uint32_t timeout_ms);
+
+/* Closes the opened peer slabs; fused launches fail until the next attach. */
+int sieve_peer_detach(void);
+
+/* Number of fused launches since the last attach (launch e uses slab
+ * parity e & 1; slot layout in csrc/peer.cuh). */
+uint64_t sieve_peer_epoch(void);
+
+/* As sieve_stats_async on this rank's [lo, hi), then result[0..1] = the
+ * sums over all attached ranks of their (count, sum mod 2^64).  A rank
+ * whose range holds no odd slot still takes part (a one-thread kernel).
+ * SIEVE_EINVAL when no peers are attached. */
+int sieve_stats_allreduce_async(uint64_t lo, uint64_t hi, const uint32_t *primes,
+                                const uint64_t *recips, const uint32_t *nbase, uint64_t *result);
+
+/* ---------------------------------------------------------------------- */
 /* Configuration and diagnostics.                                          */
 /* ---------------------------------------------------------------------- */
 int sieve_set_device(int ordinal);

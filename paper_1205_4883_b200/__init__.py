@@ -7,6 +7,9 @@ calls.  There is no CPU fallback -- if the library or a CUDA device is
 missing, every compute call raises.
 """
 from ._abi import (  # noqa: F401
+    IPC_HANDLE_BYTES,
+    MAX_PEERS,
+    PEER_SLAB_BYTES,
     SieveError,
     base_capacity,
     base_primes_async,
@@ -25,6 +28,11 @@ from ._abi import (  # noqa: F401
     lib,
     library_path,
     modpow,
+    peer_attach,
+    peer_attach_ptrs,
+    peer_detach,
+    peer_epoch,
+    peer_slab_handle,
     prepare_base_async,
     primes,
     set_device,
@@ -32,6 +40,7 @@ from ._abi import (  # noqa: F401
     set_stream,
     shutdown,
     stats,
+    stats_allreduce_async,
     stats_async,
 )
 
@@ -40,4 +49,6 @@ __all__ = [
     "base_capacity", "base_primes_async", "prepare_base_async", "stats_async", "bitmap_async",
     "set_device", "set_stream", "get_stream", "set_options", "get_options", "shutdown",
     "kernel_launches", "lib", "library_path", "modpow", "fermat", "is_prime",
+    "peer_slab_handle", "peer_attach", "peer_attach_ptrs", "peer_detach", "peer_epoch",
+    "stats_allreduce_async", "IPC_HANDLE_BYTES", "MAX_PEERS", "PEER_SLAB_BYTES",
 ]

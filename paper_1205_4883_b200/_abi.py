@@ -72,6 +72,12 @@ def lib():
             "sieve_modpow": (ctypes.c_int, [_p, _p, _p, _u64, _p]),
             "sieve_fermat": (ctypes.c_int, [_p, _u64, _p, ctypes.c_uint32, _p]),
             "sieve_is_prime": (ctypes.c_int, [_p, _u64, _p]),
+            "sieve_peer_slab_handle": (ctypes.c_int, [_p]),
+            "sieve_peer_attach": (ctypes.c_int, [_p, ctypes.c_int, ctypes.c_int, ctypes.c_uint32]),
+            "sieve_peer_attach_ptrs": (ctypes.c_int, [_p, ctypes.c_int, ctypes.c_int, ctypes.c_uint32]),
+            "sieve_peer_detach": (ctypes.c_int, []),
+            "sieve_peer_epoch": (_u64, []),
+            "sieve_stats_allreduce_async": (ctypes.c_int, [_u64, _u64, _p, _p, _p, _p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -168,6 +174,46 @@ def stats_async(lo: int, hi: int, primes_t, recips_t, nbase_t, result_t) -> None
 def bitmap_async(lo: int, hi: int, primes_t, recips_t, nbase_t, out_t, result_t) -> None:
     _check(lib().sieve_bitmap_async(lo, hi, _ptr(primes_t), _ptr(recips_t), _ptr(nbase_t),
                                     _ptr(out_t), _ptr(result_t)))
+
+
+# ---- all-reduce fused into the sieve over peer memory ----
+IPC_HANDLE_BYTES = 64
+MAX_PEERS = 64
+PEER_SLAB_BYTES = 2 * MAX_PEERS * 32
+
+
+def peer_slab_handle() -> bytes:
+    """This process's slab (allocated once) as a CUDA IPC handle."""
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(lib().sieve_peer_slab_handle(ctypes.addressof(h)))
+    return h.raw
+
+
+def peer_attach(handles: list[bytes], rank: int, timeout_ms: int = 0) -> None:
+    """Open the peers' slabs (handles in rank order, this rank's ignored)."""
+    if any(len(h) != IPC_HANDLE_BYTES for h in handles):
+        raise ValueError("every handle must be 64 bytes")
+    buf = ctypes.create_string_buffer(b"".join(handles), IPC_HANDLE_BYTES * len(handles))
+    _check(lib().sieve_peer_attach(ctypes.addressof(buf), len(handles), rank, timeout_ms))
+
+
+def peer_attach_ptrs(slabs, rank: int, timeout_ms: int = 0) -> None:
+    """Attach device slabs of this process (tensors or raw addresses, rank order)."""
+    arr = (ctypes.c_void_p * len(slabs))(*[s if isinstance(s, int) else s.data_ptr() for s in slabs])
+    _check(lib().sieve_peer_attach_ptrs(arr, len(slabs), rank, timeout_ms))
+
+
+def peer_detach() -> None:
+    _check(lib().sieve_peer_detach())
+
+
+def peer_epoch() -> int:
+    return int(lib().sieve_peer_epoch())
+
+
+def stats_allreduce_async(lo: int, hi: int, primes_t, recips_t, nbase_t, result_t) -> None:
+    _check(lib().sieve_stats_allreduce_async(lo, hi, _ptr(primes_t), _ptr(recips_t),
+                                             _ptr(nbase_t), _ptr(result_t)))
 
 
 # ---- SURVEY.md 8(f) F2: Alg. 2, Alg. 3, deterministic Miller-Rabin ----------

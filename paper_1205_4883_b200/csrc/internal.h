@@ -148,6 +148,13 @@ struct SieveParams {
   uint64_t list_cap;    // entries list may hold (later primes are counted, not written)
   unsigned long long *lflags;  // [nseg]
   uint32_t lepoch;
+  // F4 (count mode; peers == nullptr: off): the all-reduce of (count, sum)
+  // over `world` GPUs fused into the last CTA (peer.cuh).  peers[q] is rank
+  // q's slab, P2P-mapped into this process; pepoch numbers the fused launch.
+  unsigned long long *const *peers;
+  uint64_t pepoch;
+  uint64_t timeout_ns;
+  uint32_t world, rank;
 };
 
 // Diagnostic flag: skip step A4/A5 (wheel init + count/write-back only), to
@@ -172,6 +179,11 @@ cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64
                            uint32_t cap, cudaStream_t s);
 cudaError_t launch_item_ends(BatchItem *items, uint64_t n, const uint32_t *primes,
                              const uint32_t *nbase, cudaStream_t s);
+// peer.cu: the fused all-reduce alone, for a rank whose
+// block holds no odd slot (it still publishes, the peers wait for it)
+cudaError_t launch_peer_only(unsigned long long *const *peers, uint32_t world, uint32_t rank,
+                             uint64_t epoch, uint64_t timeout_ns, uint64_t count, uint64_t sum,
+                             uint64_t *result, cudaStream_t s);
 // primality.cu (Alg. 2, Alg. 3, deterministic Miller-Rabin)
 cudaError_t launch_modpow(const uint64_t *a, const uint64_t *b, const uint64_t *c, uint64_t n,
                           uint64_t *out, cudaStream_t s);

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "peer.cuh"
 
 namespace sv {
 
@@ -919,6 +920,12 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     block_sum2(c, sm, red);
     if (threadIdx.x == 0) {
       if (P.add_two) { c += 1; sm += 2; }
+      // F4: the cross-GPU all-reduce, fused (peer.cuh); sentinel on timeout
+      if (MODE == kCount && P.peers) {
+        const ulonglong2 t = peer_allreduce(P.peers, P.world, P.rank, P.pepoch, P.timeout_ns, c, sm);
+        c = t.x;
+        sm = t.y;
+      }
       P.result[0] = c;
       P.result[1] = sm;
       *P.done = 0u;  // ready for the next launch

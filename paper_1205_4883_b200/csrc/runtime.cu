@@ -23,6 +23,7 @@
 
 #include "../../include/sieve.h"
 #include "internal.h"
+#include "peer.cuh"
 
 namespace {
 
@@ -133,6 +134,16 @@ struct Ctx {
   uint64_t *h_res = nullptr;  // pinned [2]
   unsigned long long *prof = nullptr;  // diagnostics: phase-cycle counters
   uint32_t flags = 0;                  // diagnostics: sv::kFlagSkipMarking
+  // F4 fused all-reduce (peer.cuh): this process's slab, the peers' slabs
+  // opened from their IPC handles, and the device array of all ranks' slabs
+  struct Peers {
+    unsigned long long *slab = nullptr;  // own slab (library-allocated, IPC-exported)
+    std::vector<void *> opened;          // peer slabs opened by sieve_peer_attach
+    DevBuf<unsigned long long *> ptrs;   // [world]
+    uint32_t world = 0, rank = 0;        // world == 0: not attached
+    uint64_t epoch = 0;                  // fused launches since the attach
+    uint64_t timeout_ns = 0;
+  } peer;
   cudaStream_t stream() const { return user_set ? user : own; }
 };
 
@@ -389,6 +400,46 @@ int bitmap_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, 
   sp.out_words = P.words;
   sp.out_vec4 = ((uintptr_t)out & 15u) == 0 ? 1u : 0u;
   return run_sieve(sv::kBitmap, sp, P.nseg);
+}
+
+// F4: count/sum of this rank's [lo, hi) summed over every attached rank, the
+// all-reduce done inside the sieve kernel's last CTA (peer.cuh)
+int stats_allreduce_async(const Plan &P, const uint32_t *primes, const uint64_t *recips,
+                          const uint32_t *nbase, uint64_t *result) {
+  auto &pe = g.peer;
+  pe.epoch += 1;
+  if (P.nbits == 0) {  // no sieve launch: publish (0, 0) or (1, 2) alone
+    CUDA_TRY(sv::launch_peer_only(pe.ptrs.p, pe.world, pe.rank, pe.epoch, pe.timeout_ns,
+                                  P.two ? 1 : 0, P.two ? 2 : 0, result, g.stream()));
+    g_launches += 1;
+    return 0;
+  }
+  sv::SieveParams sp = params_for(P, primes, recips, nbase, result);
+  sp.peers = pe.ptrs.p;
+  sp.pepoch = pe.epoch;
+  sp.timeout_ns = pe.timeout_ns;
+  sp.world = pe.world;
+  sp.rank = pe.rank;
+  return run_sieve(sv::kCount, sp, P.nseg);
+}
+
+void peer_detach() {
+  for (void *q : g.peer.opened)
+    if (q) cudaIpcCloseMemHandle(q);
+  g.peer.opened.clear();
+  g.peer.world = 0;
+  g.peer.rank = 0;
+}
+
+int peer_attach(unsigned long long *const *slabs, uint32_t world, uint32_t rank,
+                uint32_t timeout_ms) {
+  TRY(g.peer.ptrs.ensure(world));
+  CUDA_TRY(cudaMemcpy(g.peer.ptrs.p, slabs, world * sizeof(void *), cudaMemcpyHostToDevice));
+  g.peer.world = world;
+  g.peer.rank = rank;
+  g.peer.epoch = 0;
+  g.peer.timeout_ns = (uint64_t)(timeout_ms ? timeout_ms : 10000) * 1000000ull;
+  return 0;
 }
 
 bool is_device_ptr(const void *p) {
@@ -716,6 +767,87 @@ int sieve_bitmap_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const u
   return bitmap_async(P, primes, recips, nbase, out, result);
 }
 
+int sieve_peer_slab_handle(void *handle_out) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!handle_out) return fail(SIEVE_EINVAL, "NULL handle_out");
+  TRY(ensure_ready());
+  if (!g.peer.slab) {
+    CUDA_TRY(cudaMalloc(&g.peer.slab, sv::kPeerSlabBytes));
+    CUDA_TRY(cudaMemset(g.peer.slab, 0, sv::kPeerSlabBytes));
+  }
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, g.peer.slab));
+  static_assert(sizeof h == SIEVE_IPC_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+  memcpy(handle_out, &h, sizeof h);
+  return 0;
+}
+
+int sieve_peer_attach(const void *handles, int world, int rank, uint32_t timeout_ms) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!handles) return fail(SIEVE_EINVAL, "NULL handles");
+  if (world < 1 || world > SIEVE_MAX_PEERS || rank < 0 || rank >= world)
+    return fail(SIEVE_EINVAL, "world %d / rank %d out of range (1 <= world <= %d)", world, rank,
+                SIEVE_MAX_PEERS);
+  TRY(ensure_ready());
+  if (!g.peer.slab) return fail(SIEVE_EINVAL, "sieve_peer_slab_handle was not called");
+  CUDA_TRY(cudaStreamSynchronize(g.stream()));
+  peer_detach();
+  std::vector<unsigned long long *> slabs(world, nullptr);
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) {
+      slabs[q] = g.peer.slab;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const char *)handles + (size_t)q * SIEVE_IPC_HANDLE_BYTES, sizeof h);
+    void *ptr = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      peer_detach();
+      return fail(SIEVE_ECUDA, "cudaIpcOpenMemHandle(rank %d) failed: %s", q, cudaGetErrorString(e));
+    }
+    g.peer.opened.push_back(ptr);
+    slabs[q] = (unsigned long long *)ptr;
+  }
+  // stale epochs of an earlier attach must not match the new ones
+  CUDA_TRY(cudaMemset(g.peer.slab, 0, sv::kPeerSlabBytes));
+  return peer_attach(slabs.data(), (uint32_t)world, (uint32_t)rank, timeout_ms);
+}
+
+int sieve_peer_attach_ptrs(void *const *slabs, int world, int rank, uint32_t timeout_ms) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!slabs) return fail(SIEVE_EINVAL, "NULL slabs");
+  if (world < 1 || world > SIEVE_MAX_PEERS || rank < 0 || rank >= world)
+    return fail(SIEVE_EINVAL, "world %d / rank %d out of range (1 <= world <= %d)", world, rank,
+                SIEVE_MAX_PEERS);
+  for (int q = 0; q < world; ++q)
+    if (!slabs[q]) return fail(SIEVE_EINVAL, "NULL slab for rank %d", q);
+  TRY(ensure_ready());
+  CUDA_TRY(cudaStreamSynchronize(g.stream()));
+  peer_detach();
+  return peer_attach((unsigned long long *const *)slabs, (uint32_t)world, (uint32_t)rank,
+                     timeout_ms);
+}
+
+int sieve_peer_detach(void) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.ready) CUDA_TRY(cudaStreamSynchronize(g.stream()));
+  peer_detach();
+  return 0;
+}
+
+uint64_t sieve_peer_epoch(void) { return g.peer.epoch; }
+
+int sieve_stats_allreduce_async(uint64_t lo, uint64_t hi, const uint32_t *primes,
+                                const uint64_t *recips, const uint32_t *nbase, uint64_t *result) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  TRY(validate(lo, hi));
+  if (!primes || !recips || !nbase || !result) return fail(SIEVE_EINVAL, "NULL buffer");
+  if (g.peer.world == 0) return fail(SIEVE_EINVAL, "no peers attached (sieve_peer_attach)");
+  TRY(ensure_ready());
+  return stats_allreduce_async(make_plan(lo, hi), primes, recips, nbase, result);
+}
+
 int sieve_set_device(int ordinal) {
   std::lock_guard<std::mutex> lk(g.mu);
   int ndev = 0;
@@ -795,6 +927,10 @@ void sieve_shutdown(void) {
   g.partials.release(); g.done.release(); g.result.release(); g.bitmap.release();
   g.list.release(); g.items.release(); g.bres.release();
   g.buckets.release(); g.kflags.release(); g.lflags.release(); g_f2.buf.release();
+  peer_detach();
+  g.peer.ptrs.release();
+  if (g.peer.slab) cudaFree(g.peer.slab);
+  g.peer.slab = nullptr;
   if (g.h_res) cudaFreeHost(g.h_res);
   g.h_res = nullptr;
   if (g.own) cudaStreamDestroy(g.own);

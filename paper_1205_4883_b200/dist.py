@@ -12,7 +12,11 @@ one NVSwitch box:
               data from other nodes becomes a single NCCL broadcast)
   sieve     : every rank runs the segmented sieve on its block (CUDA, C ABI)
   gather    : one all-reduce of u64[2] = {count, sum}; two's-complement int64
-              addition is bit-identical to u64 addition mod 2^64.
+              addition is bit-identical to u64 addition mod 2^64.  With
+              attach_peers() done (F4) that all-reduce happens INSIDE the
+              sieve kernel: its last CTA writes the rank's result into every
+              peer's slab over NVLink and sums its own (csrc/peer.cuh) --
+              no NCCL launch on the count path.
 
 The compute callables default to the CUDA library; tests may inject others
 to exercise this host logic with the gloo backend on CPU.
@@ -52,6 +56,28 @@ def block_of(lo: int, hi: int, rank: int, world: int) -> tuple[int, int]:
     return edge(rank), edge(rank + 1)
 
 
+class _LibraryStreamOrder:
+    """Orders the library's stream (sieve_set_stream, or its own) after
+    torch's current stream on entry -- the buffers were allocated/filled
+    there -- and torch's current stream after the library's on exit, so the
+    caller can read the result on its stream.  A no-op when they coincide."""
+
+    def __enter__(self):
+        import torch
+        import paper_1205_4883_b200 as sv
+        self.cur = torch.cuda.current_stream()
+        h = sv.get_stream()
+        self.lib = None if h in (0, self.cur.cuda_stream) else torch.cuda.ExternalStream(h)
+        if self.lib is not None:
+            self.lib.wait_stream(self.cur)
+        return self
+
+    def __exit__(self, *exc):
+        if self.lib is not None:
+            self.cur.wait_stream(self.lib)
+        return False
+
+
 class CudaBackend:
     """The product compute path: the C-ABI library on the current device."""
 
@@ -61,11 +87,58 @@ class CudaBackend:
 
     def base_primes(self, r, base):
         import paper_1205_4883_b200 as sv
-        sv.base_primes_async(r, base.primes, base.recips, base.nbase)
+        with _LibraryStreamOrder():
+            sv.base_primes_async(r, base.primes, base.recips, base.nbase)
 
     def stats(self, a, b, base, result):
         import paper_1205_4883_b200 as sv
-        sv.stats_async(a, b, base.primes, base.recips, base.nbase, result)
+        with _LibraryStreamOrder():
+            sv.stats_async(a, b, base.primes, base.recips, base.nbase, result)
+
+    def stats_allreduce(self, a, b, base, result):
+        import paper_1205_4883_b200 as sv
+        with _LibraryStreamOrder():
+            sv.stats_allreduce_async(a, b, base.primes, base.recips, base.nbase, result)
+
+    def peer_handle(self) -> bytes:
+        import paper_1205_4883_b200 as sv
+        return sv.peer_slab_handle()
+
+    def peer_attach(self, handles, rank, timeout_ms):
+        import paper_1205_4883_b200 as sv
+        sv.peer_attach(handles, rank, timeout_ms)
+
+    def peer_detach(self):
+        import paper_1205_4883_b200 as sv
+        sv.peer_detach()
+
+
+# groups attached for the fused all-reduce (F4): id(group) -> world
+_ATTACHED: dict = {}
+SENTINEL = (1 << 64) - 1
+
+
+def attach_peers(group=None, timeout_ms: int = 10000, backend=None) -> bool:
+    """F4 setup, collective over `group`: every rank exports its slab's CUDA
+    IPC handle, the handles are all-gathered over the host in rank order and
+    every rank opens its peers' slabs; a barrier makes every slab zeroed
+    before anyone's first fused launch.  Later stats(..., fused=True) calls
+    on this group all-reduce inside the sieve kernel."""
+    import torch.distributed as dist
+    be = backend if backend is not None else CudaBackend()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    mine = be.peer_handle()
+    if world > 1:
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+    else:
+        handles = [mine]
+    be.peer_attach(handles, rank, timeout_ms)
+    if world > 1:
+        dist.barrier(group=group)
+    _ATTACHED[id(group)] = world
+    return True
 
 
 def u64_to_i64(x: int) -> int:
@@ -97,11 +170,20 @@ def alloc_base(cap: int, device) -> BaseBuffers:
     return BaseBuffers(packed, recips, primes, nbase, cap)
 
 
+def detach_peers(group=None, backend=None) -> None:
+    """Undo attach_peers: later stats() calls on `group` use NCCL again."""
+    _ATTACHED.pop(id(group), None)
+    be = backend if backend is not None else CudaBackend()
+    be.peer_detach()
+
+
 def stats(lo: int, hi: int, group=None, broadcast: bool = True, base: BaseBuffers | None = None,
-          result=None, sync: bool = True, backend=None, device=None):
+          result=None, sync: bool = True, backend=None, device=None, fused: bool | None = None):
     """pi-count and prime sum of [lo, hi) over all ranks of `group` (public
     multi-GPU API).  Returns (count, sum mod 2^64) on every rank when sync,
-    else the device result tensor (int64[2], already all-reduced)."""
+    else the device result tensor (int64[2], already all-reduced).
+    fused (default: whether attach_peers(group) was done): the all-reduce
+    runs inside the sieve kernel over peer memory (F4) instead of NCCL."""
     import torch
     import torch.distributed as dist
 
@@ -119,13 +201,21 @@ def stats(lo: int, hi: int, group=None, broadcast: bool = True, base: BaseBuffer
     if world > 1 and broadcast:
         dist.broadcast(base.packed, src=0, group=group)
     a, b = block_of(lo, hi, rank, world)
-    be.stats(a, b, base, result)
-    if world > 1:
-        dist.all_reduce(result, op=dist.ReduceOp.SUM, group=group)
+    if fused is None:
+        fused = _ATTACHED.get(id(group)) == world
+    if fused:
+        be.stats_allreduce(a, b, base, result)
+    else:
+        be.stats(a, b, base, result)
+        if world > 1:
+            dist.all_reduce(result, op=dist.ReduceOp.SUM, group=group)
     if not sync:
         return result
     h = result.cpu().tolist()
-    return i64_to_u64(h[0]), i64_to_u64(h[1])
+    c, s = i64_to_u64(h[0]), i64_to_u64(h[1])
+    if fused and c == SENTINEL:
+        raise RuntimeError("fused all-reduce timed out waiting for a peer (sieve_peer_attach)")
+    return c, s
 
 
 # ---------------------------------------------------------------- batch / LPT
@@ -234,7 +324,8 @@ class CudaGatherBackend:
         n = sv.bitmap_words(a, b)
         out = torch.zeros(max(n, 1), dtype=torch.int32, device=device)
         if n:
-            sv.bitmap(a, b, out=out)
+            with _LibraryStreamOrder():
+                sv.bitmap(a, b, out=out)
         return out[:n]
 
     def primes(self, a, b, device):
@@ -243,7 +334,8 @@ class CudaGatherBackend:
         n = sv.count(a, b)
         out = torch.zeros(max(n, 1), dtype=torch.int64, device=device)
         if n:
-            sv.primes(a, b, cap=n, out=out)
+            with _LibraryStreamOrder():
+                sv.primes(a, b, cap=n, out=out)
         return out[:n]
 
 

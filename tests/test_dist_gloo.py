@@ -1,12 +1,16 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the multi-GPU host logic
 in paper_1205_4883_b200/dist.py: block partition, the packed base-prime
 broadcast, the u64-as-int64 all-reduce, the LPT batch assignment with its
-all_gather reassembly, and the F1 gather of per-rank bitmaps and lists with
-the decomposable bitmap checksum.  The per-rank compute is injected (a CPU stand-in
+all_gather reassembly, the F1 gather of per-rank bitmaps and lists with
+the decomposable bitmap checksum, and the F4 fused all-reduce's protocol
+(csrc/peer.cuh: slab slots, epochs, parity double buffering) between real
+processes on shared memory.  The per-rank compute is injected (a CPU stand-in
 built on the oracle) because this container has no GPU; the CUDA backend is
 the default in the product path and is exercised by the -m gpu tests."""
 import os
 import socket
+import tempfile
+import time
 
 import numpy as np
 import pytest
@@ -67,7 +71,55 @@ class OracleGatherBackend:
         return torch.from_numpy(oracle.primes(a, b).view(np.int64).copy())
 
 
-def _worker(rank, world, port, q):
+class SlabSimBackend(OracleBackend):
+    """CPU stand-in for the F4 fused all-reduce (test only): each rank's slab
+    is a shared file mapping (its path is the "IPC handle"), and
+    stats_allreduce follows csrc/peer.cuh step by step -- publish (count,
+    sum) then the epoch into slot [e & 1][rank] of every slab, then wait for
+    epoch e in every slot [e & 1][*] of its own slab and sum.  x86 stores are
+    ordered, standing in for the kernel's release/acquire pair."""
+
+    def __init__(self, tmpdir, rank):
+        self.path = os.path.join(tmpdir, f"slab{rank}")
+        np.zeros(512, dtype=np.uint64).tofile(self.path)
+        self.views = None
+
+    def peer_handle(self):
+        return self.path.encode().ljust(64, b"\0")
+
+    def peer_attach(self, handles, rank, timeout_ms):
+        self.handles = handles
+        self.rank, self.world, self.epoch = rank, len(handles), 0
+        self.views = [np.memmap(h.rstrip(b"\0").decode(), dtype=np.uint64, mode="r+", shape=(512,))
+                      for h in handles]
+
+    def peer_detach(self):
+        self.views = None
+
+    def stats_allreduce(self, a, b, base, result):
+        self.epoch += 1
+        e = self.epoch
+        c, s = oracle.stats(a, b, 1)
+        par = (e & 1) * 64
+        for v in self.views:
+            i = 4 * (par + self.rank)
+            v[i], v[i + 1] = c, s
+            v[i + 2] = e
+        mine = self.views[self.rank]
+        tc = ts = 0
+        for q in range(self.world):
+            i = 4 * (par + q)
+            t0 = time.time()
+            while int(mine[i + 2]) != e:
+                assert time.time() - t0 < 60, "peer never published"
+                time.sleep(0)
+            tc += int(mine[i])
+            ts += int(mine[i + 1])
+        result[0] = D.u64_to_i64(tc & MASK64)
+        result[1] = D.u64_to_i64(ts & MASK64)
+
+
+def _worker(rank, world, port, q, tmpdir=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -90,6 +142,20 @@ def _worker(rank, world, port, q):
             words, cs = D.gather_bitmap(lo, hi, backend=gb, device=cpu)
             lst = D.gather_primes(lo, hi, backend=gb, device=cpu)
             out[("F1", lo, hi)] = (words.numpy().view(np.uint32).tolist(), cs, lst.numpy().tolist())
+        # F4: the fused all-reduce protocol between the two processes; random
+        # per-rank delays let one rank run ahead into the other parity
+        sim = SlabSimBackend(tmpdir, rank)
+        D.attach_peers(backend=sim)
+        out["handles"] = [h.rstrip(b"\0").decode() for h in sim.handles]
+        rng = np.random.default_rng(rank + 7)
+        for k in range(40):
+            lo, hi = 10**6 * k + k, 10**6 * k + 6 * 10**4 + 3 * k
+            if rng.random() < 0.5:
+                time.sleep(rng.random() * 0.02)
+            out[("F4", lo, hi)] = D.stats(lo, hi, backend=sim, device=cpu)
+        out[("F4", 9, 9)] = D.stats(9, 9, backend=sim, device=cpu)
+        out["epochs"] = sim.epoch
+        D.detach_peers(backend=sim)
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -99,7 +165,8 @@ def test_two_rank_gloo_stats_batch_and_wrap():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    tmpdir = tempfile.mkdtemp(prefix="slabs")
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, tmpdir)) for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=300) for _ in ps)
@@ -116,8 +183,12 @@ def test_two_rank_gloo_stats_batch_and_wrap():
             assert words == obm.tolist(), key                     # gathered bitmap == whole bitmap
             assert cs == D.bitmap_checksum(obm), key              # all-reduced decomposable checksum
             assert lst == oracle.primes(lo, hi).tolist(), key     # gathered list == whole list
+        elif isinstance(key, tuple) and key[0] == "F4":
+            assert val == oracle.stats(*key[1:]), key          # one reduction, whole range
         elif isinstance(key, tuple):
             assert val == oracle.stats(*key), key
+    assert r["handles"] == [os.path.join(tmpdir, "slab0"), os.path.join(tmpdir, "slab1")]
+    assert r["epochs"] == 41
     lo5, hi5 = inputs.config5_intervals(64)
     oc, os_ = oracle.batch(lo5, hi5)
     assert r["batch"] == (oc.tolist(), os_.tolist())
