@@ -131,7 +131,7 @@ struct SieveParams {
   unsigned int *done;      // last-block-done ticket (self-resetting)
   uint64_t *result;        // [2] count, sum mod 2^64 (batch: [2 * nintervals])
   const BatchItem *items;  // batch mode
-  unsigned long long *prof;  // optional phase-cycle counters (diagnostics), [104]
+  unsigned long long *prof;  // optional phase-cycle counters + timeline (diagnostics), [112]
   uint32_t flags;            // diagnostics: kFlagSkipMarking
   // step A5 buckets (nullptr: off).  CTA c sieves the contiguous segments
   // [c nseg / grid, (c+1) nseg / grid); bucket (c, slot, warp) holds capw

@@ -816,9 +816,16 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   __shared__ uint32_t s_wc[33];            // list mode: warp counts / offsets, segment total
   __shared__ unsigned long long s_off;     // list mode: the segment's place in the list
 
+  // diagnostics timeline (P.prof[104..109], globaltimer ns; min as max of ~t)
+  if (P.prof && threadIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    atomicMax(P.prof + 104, ~t);
+    atomicMax(P.prof + 105, t);
+  }
   for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
   compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
   __syncthreads();
+  if (P.prof && threadIdx.x == 0) atomicMax(P.prof + 106, global_ns());
 
   unsigned long long cnt = 0, sum = 0;
   // segments round robin; with the buckets of step A5 a range is sieved in
@@ -901,6 +908,11 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
 
   // per-CTA partial, then the last CTA to finish reduces all partials in a
   // fixed order (deterministic) and writes the result.
+  if (P.prof && threadIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    atomicMax(P.prof + 107, t);
+    atomicMax(P.prof + 109, ~t);
+  }
   block_sum2(cnt, sum, red);
   if (threadIdx.x == 0) {
     P.partials[2 * blockIdx.x] = cnt;
@@ -929,6 +941,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       P.result[0] = c;
       P.result[1] = sm;
       *P.done = 0u;  // ready for the next launch
+      if (P.prof) atomicMax(P.prof + 108, global_ns());
     }
   }
 }

@@ -254,16 +254,21 @@ int grid_for(uint64_t nseg);
 
 // Step A1 segment size: the range is cut into w waves of G segments (G the
 // persistent grid), w = ceil(B / (S_max G)), with S = ceil(B / (w G)) rounded
-// up to 8 KiB of slots: every CTA sieves the same number of equal segments
-// (a 2.48-wave launch would otherwise run 3 waves, the last half empty), and
-// a small range still spreads over all SMs.  S <= S_max (option segment_kb).
+// up to a T-layout block (1024 slots): every CTA sieves the same number of
+// equal segments (a 2.48-wave launch would otherwise run 3 waves, the last
+// half empty; coarser rounding, e.g. to 64 Ki slots, leaves up to w - 1
+// segments short of w G and their CTAs idle for a whole segment), and a small
+// range still spreads over all SMs.  65536 <= S <= S_max (option segment_kb).
 uint64_t balanced_sbits(uint64_t nbits) {
   const uint64_t smax = seg_bits();
   if (nbits == 0) return smax;
   const uint64_t G = (uint64_t)grid_for(~0ull);
   const uint64_t waves = (nbits + smax * G - 1) / (smax * G);
   uint64_t S = (nbits + waves * G - 1) / (waves * G);
-  S = (S + 65535) / 65536 * 65536;
+#ifndef SIEVE_SROUND
+#define SIEVE_SROUND 1024
+#endif
+  S = (S + SIEVE_SROUND - 1) / SIEVE_SROUND * SIEVE_SROUND;
   return std::min(smax, std::max<uint64_t>(S, 65536));
 }
 
