@@ -198,15 +198,17 @@ void sieve_shutdown(void);
 /* Number of kernels this library launched since load (evidence counter). */
 uint64_t sieve_kernel_launches(void);
 
-/* Diagnostics: when dev_counters (device, 112 x uint64, zeroed by the caller)
+/* Diagnostics: when dev_counters (device, 120 x uint64, zeroed by the caller)
  * is non-NULL, later sieve launches add SM-clock cycles per phase:
  * [0] wheel init, [1] marking, [2] count/write-back (CTA level, summed over
  * segments), [3] small-, [4] medium-, [5] large-prime marking (per warp,
  * summed over warps), [6] segments, [8..103] per-warp region cycles, and a
  * globaltimer timeline of the count/bitmap kernel (ns): [104] ~min CTA
  * entry, [105] max entry, [106] max end of prologue, [107] max end of
- * sieving, [108] result written, [109] ~min end of sieving.  The buffer
- * must hold 112 entries.  NULL disables (the default). */
+ * sieving, [108] result written, [109] ~min end of sieving; of the base-
+ * prime kernel: [112] ~min entry, [113] small primes, [114] slice marked,
+ * [115] list offset known, [116] end (max over CTAs).  The buffer must hold
+ * 120 entries.  NULL disables (the default). */
 int sieve_debug_set_profile(uint64_t *dev_counters);
 
 /* Diagnostics: flags for later launches.  1 = skip the marking step (A4/A5):

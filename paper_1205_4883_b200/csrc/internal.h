@@ -131,7 +131,7 @@ struct SieveParams {
   unsigned int *done;      // last-block-done ticket (self-resetting)
   uint64_t *result;        // [2] count, sum mod 2^64 (batch: [2 * nintervals])
   const BatchItem *items;  // batch mode
-  unsigned long long *prof;  // optional phase-cycle counters + timeline (diagnostics), [112]
+  unsigned long long *prof;  // optional phase-cycle counters + timelines (diagnostics), [120]
   uint32_t flags;            // diagnostics: kFlagSkipMarking
   // step A5 buckets (nullptr: off).  CTA c sieves the contiguous segments
   // [c nseg / grid, (c+1) nseg / grid); bucket (c, slot, warp) holds capw
@@ -173,7 +173,7 @@ cudaError_t launch_sieve(int ng, int mode, const SieveParams &p, int grid, int t
 cudaError_t set_sieve_smem_limits(size_t smem);
 cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64_t *recips,
                                uint32_t cap, uint32_t *nbase, uint64_t *flags, uint32_t epoch,
-                               int nsm, cudaStream_t s);
+                               int nsm, unsigned long long *prof, cudaStream_t s);
 uint32_t base_slices(uint32_t r);  // look-back flags the base-prime kernel needs
 cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
                            uint32_t cap, cudaStream_t s);

@@ -948,87 +948,146 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
 
 // ---------------------------------------------------------------------------
 // A2: base primes, the odd primes <= r (r <= 2^24), ascending, with their
-// Barrett reciprocals.  The odd numbers <= r are cut into slices of
-// kSliceBits; a CTA of kBaseThreads threads takes slices b, b + G, ... (all
-// CTAs resident).  Per slice: the odd primes q <= sqrt(r) (computed once per
-// CTA by trial division, kept in shared memory) mark their odd multiples
-// >= q^2 in a shared bitmap (thread t owns word t); the block counts the
-// survivors, publishes the slice's count, and finds the slice's place in the
-// list by a decoupled look-back over the earlier slices' published counts
-// (flags tagged with the launch's epoch, so no reset between launches); then
-// the primes are written in order (block scan of the per-thread counts).
+// Barrett reciprocals.  The odd numbers n = 2i + 1 <= r (i >= 1) are cut into
+// slices of kSliceBits; a CTA of kBaseThreads threads takes slices b, b + G,
+// ... (all CTAs resident).  Latency-shaped (the kernel runs before the sieve
+// on a handful of SMs, so its critical path is the step's):
+//  * the odd primes q <= sqrt(r) (<= 4096) come from a 2048-bit mini-sieve by
+//    the primes <= 61 (one word per thread of the first two warps), kept in
+//    shared memory;
+//  * per slice, thread t builds word t from the periodic patterns of the
+//    primes 3..31 (a shifted constant per prime: no atomics), then one warp
+//    per remaining prime q > 31 marks its odd multiples >= q^2 (lanes on
+//    consecutive hits);
+//  * the block counts the survivors, publishes the slice's count and finds
+//    the slice's place in the list by a decoupled look-back over the earlier
+//    slices (flags tagged with the launch's epoch: no reset between launches);
+//  * the slice's primes are staged in shared memory in order, then written
+//    with their reciprocals by all threads (coalesced, independent).
+// A pattern prime q itself (bit (q - 3) / 2 of slice 0) is cleared again: the
+// patterns mark every odd multiple of q, which is composite except q.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kBaseThreads = 256;
 constexpr uint32_t kSliceBits = 32u * kBaseThreads;  // one word per thread
 constexpr uint32_t kMaxSmall = 1024;                 // odd primes <= 4096 number 563
+constexpr uint32_t kMaxSlicePrimes = 2048;           // primes among 8192 odd n: <= 1899 (slice 0)
+constexpr int kNumPat = 10;                          // pattern primes 3..31
 
 __device__ __forceinline__ uint64_t make_flag(uint32_t epoch, uint64_t v, uint64_t st) {
   return ((uint64_t)epoch << 48) | (v << 2) | st;
 }
 
+// bit b of the result is set iff 2(I + b) + 1 is an odd multiple of a pattern
+// prime 3..31: for q, the bits b = ((q-1)/2 - I) mod q + k q
+__device__ __forceinline__ uint32_t pattern_word(uint32_t I) {
+  constexpr uint32_t kQ[kNumPat] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31};
+  uint32_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kNumPat; ++k) {
+    const uint32_t q = kQ[k], h = (q - 1u) / 2u;
+    uint32_t pat = 0;  // bits 0, q, 2q, ... < 32 (constant-folded)
+    for (uint32_t b = 0; b < 32u; b += q) pat |= 1u << b;
+    const uint32_t t = I % q;
+    const uint32_t f = h >= t ? h - t : h + q - t;
+    v |= pat << f;
+  }
+  return v;
+}
+
 __global__ void __launch_bounds__(kBaseThreads) k_base_primes(uint32_t r, uint32_t rs, uint32_t *primes,
                                                               uint64_t *recips, uint32_t cap,
                                                               uint32_t *nbase, uint64_t *flags,
-                                                              uint32_t epoch) {
+                                                              uint32_t epoch, unsigned long long *prof) {
   __shared__ uint32_t bm[kSliceBits / 32];
   __shared__ uint32_t sp[kMaxSmall];
-  __shared__ uint32_t s_j0[kMaxSmall];
+  __shared__ uint32_t s_list[kMaxSlicePrimes];
   __shared__ uint32_t s_w[kBaseThreads / 32];
   __shared__ uint32_t s_nsp;
   __shared__ unsigned long long s_off;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x >> 5;
-  if (tid == 0) s_nsp = 0;
-  __syncthreads();
-  // odd primes q <= rs, ascending: rounds of blockDim candidates, ballot compaction
-  for (uint32_t base = 3; base <= rs; base += 2u * blockDim.x) {
-    const uint32_t q = base + 2u * tid;
-    bool isp = q <= rs;
-    for (uint32_t d = 3; isp && d * d <= q; d += 2)
-      if (q % d == 0) isp = false;
-    const uint32_t bal = __ballot_sync(0xffffffffu, isp);
-    if (lane == 0) s_w[warp] = __popc(bal);
-    __syncthreads();
-    uint32_t off = s_nsp;
-    for (uint32_t w = 0; w < warp; ++w) off += s_w[w];
-    off += __popc(bal & ((1u << lane) - 1u));
-    if (isp && off < kMaxSmall) sp[off] = q;
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t t = 0;
-      for (uint32_t w = 0; w < nw; ++w) t += s_w[w];
-      s_nsp += t;
-    }
-    __syncthreads();
-  }
-  const uint32_t nsp = min(s_nsp, kMaxSmall);
+  // diagnostics timeline (prof[112..116], globaltimer ns; min as max of ~t)
+  auto stamp = [&](int k) {
+    if (prof && tid == 0) atomicMax(prof + k, k == 112 ? ~global_ns() : global_ns());
+  };
+  stamp(112);
 
-  // odd n = 2i + 1, i in [1, imax]; slice k covers i in [1 + k S, 1 + (k+1) S)
+  // odd primes 3 <= q <= rs (rs <= 4096): mini-sieve of i = 1..2047 (n = 2i+1)
+  // by the primes <= 61, then an ordered compaction (two warps)
+  if (warp < 2u) {
+    const uint32_t I = 1u + 32u * tid;  // first i of word tid
+    uint32_t v = pattern_word(I);
+    constexpr uint32_t big[7] = {37, 41, 43, 47, 53, 59, 61};  // at most one multiple per word
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      const uint32_t q = big[k], h = (q - 1u) / 2u, t = I % q;
+      const uint32_t f = h >= t ? h - t : h + q - t;
+      if (f < 32u) v |= 1u << f;
+    }
+    if (tid == 0) {  // the sieving primes themselves: i = (q-1)/2, bit i - 1
+      v &= ~((1u << 0) | (1u << 1) | (1u << 2) | (1u << 4) | (1u << 5) | (1u << 7) | (1u << 8) |
+             (1u << 10) | (1u << 13) | (1u << 14) | (1u << 17) | (1u << 19) | (1u << 20) |
+             (1u << 22) | (1u << 25) | (1u << 28) | (1u << 29));
+    }
+    uint32_t x = ~v;
+    // keep n = 2i + 1 <= rs: i <= (rs - 1) / 2
+    const uint32_t imax_s = rs >= 3u ? (rs - 1u) / 2u : 0u;
+    if (I > imax_s) x = 0;
+    else if (imax_s - I < 31u) x &= (2u << (imax_s - I)) - 1u;
+    const uint32_t c = __popc(x);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane == 31u) s_w[warp] = incl;
+    bm[tid] = x;  // staged: the compaction needs warp 0's total
+    bm[64u + tid] = incl - c;
+  }
+  __syncthreads();
+  if (warp < 2u) {
+    uint32_t x = bm[tid], o = bm[64u + tid] + (warp ? s_w[0] : 0u);
+    while (x) {
+      const uint32_t b = __ffs(x) - 1u;
+      x &= x - 1u;
+      if (o < kMaxSmall) sp[o] = 2u * (1u + 32u * tid + b) + 1u;
+      ++o;
+    }
+    if (tid == 0) s_nsp = s_w[0] + s_w[1];
+  }
+  __syncthreads();
+  const uint32_t nsp = min(s_nsp, kMaxSmall);
+  // first index with sp > 31 (sp holds 3, 5, ..., 31 first when rs >= 31)
+  const uint32_t m31 = min(nsp, (uint32_t)kNumPat);
+  stamp(113);
+
   const uint32_t imax = r >= 3 ? (r - 1) / 2 : 0;
   const uint32_t nslice = (imax + kSliceBits - 1) / kSliceBits;
   for (uint32_t k = blockIdx.x; k < nslice; k += gridDim.x) {
     const uint32_t i0 = 1 + k * kSliceBits;
     const uint32_t nbits = min(kSliceBits, imax - i0 + 1);
-    bm[tid] = 0;
     const uint32_t a = 2u * i0 + 1u, e = a + 2u * nbits;  // odd integers [a, e)
-    // the slice offset of every small prime's first odd multiple >= max(q^2, a),
-    // one prime per thread (the divisions run in parallel, not in the loop below)
-    for (uint32_t m = tid; m < nsp; m += blockDim.x) {
+    uint32_t v = pattern_word(i0 + 32u * tid);
+    if (k == 0 && tid == 0) {  // 3..31 are prime: bits (q - 3) / 2
+      v &= ~((1u << 0) | (1u << 1) | (1u << 2) | (1u << 4) | (1u << 5) | (1u << 7) | (1u << 8) |
+             (1u << 10) | (1u << 13) | (1u << 14));
+    }
+    bm[tid] = v;
+    __syncthreads();
+    // one warp per prime q > 31 (ascending per warp: past q^2 >= e, stop)
+    for (uint32_t m = m31 + warp; m < nsp; m += nw) {
       const uint32_t q = sp[m];
       uint32_t f = q * q;
+      if (f >= e) break;
       if (f < a) {
         f = ((a + q - 1u) / q) * q;
         if (!(f & 1u)) f += q;
       }
-      s_j0[m] = f < e ? (f - a) / 2u : kNone;
+      for (uint32_t j = (f - a) / 2u + lane * q; j < nbits; j += 32u * q)
+        atomicOr(&bm[j >> 5], 1u << (j & 31));
     }
     __syncthreads();
-    for (uint32_t m = 0; m < nsp; ++m) {  // all threads on one prime at a time
-      const uint32_t j0 = s_j0[m];
-      if (j0 == kNone) break;             // q^2 past the slice: so for every later prime
-      const uint32_t q = sp[m];
-      for (uint32_t j = j0 + tid * q; j < nbits; j += blockDim.x * q) atomicOr(&bm[j >> 5], 1u << (j & 31));
-    }
-    __syncthreads();
+    stamp(114);
     uint32_t x = ~bm[tid];
     const uint32_t vb = nbits > 32u * tid ? nbits - 32u * tid : 0u;  // valid bits of word tid
     if (vb < 32u) x &= (1u << vb) - 1u;
@@ -1066,20 +1125,27 @@ __global__ void __launch_bounds__(kBaseThreads) k_base_primes(uint32_t r, uint32
       }
       if (k == nslice - 1) *nbase = (uint32_t)min((uint64_t)cap, (uint64_t)(s_off + tot));
     }
-    __syncthreads();
-    uint64_t o = s_off + excl;
+    // stage the slice's primes in order (tot <= kMaxSlicePrimes: see above)
+    uint32_t o = excl;
     while (x) {
       const uint32_t b = __ffs(x) - 1;
       x &= x - 1;
-      const uint32_t p = a + 2u * (32u * tid + b);
-      if (o < cap) {
-        primes[o] = p;
-        recips[o] = recip_of(p);
-      }
+      if (o < kMaxSlicePrimes) s_list[o] = a + 2u * (32u * tid + b);
       ++o;
     }
-    __syncthreads();  // bm and s_w are reused by the next slice
+    __syncthreads();
+    stamp(115);
+    const uint64_t off = s_off;
+    for (uint32_t t = tid; t < min(tot, kMaxSlicePrimes); t += blockDim.x) {
+      const uint32_t p = s_list[t];
+      if (off + t < cap) {
+        primes[off + t] = p;
+        recips[off + t] = recip_of(p);
+      }
+    }
+    __syncthreads();  // bm, s_w and s_list are reused by the next slice
   }
+  stamp(116);
   if (nslice == 0 && blockIdx.x == 0 && tid == 0) *nbase = 0;
 }
 
@@ -1173,11 +1239,11 @@ uint32_t base_slices(uint32_t r) {
 
 cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64_t *recips,
                                uint32_t cap, uint32_t *nbase, uint64_t *flags, uint32_t epoch,
-                               int nsm, cudaStream_t s) {
+                               int nsm, unsigned long long *prof, cudaStream_t s) {
   const uint32_t ns = base_slices(r);
   // all CTAs resident (the look-back waits on earlier slices): <= 4 per SM
   const uint32_t grid = ns < 4u * (uint32_t)nsm ? (ns ? ns : 1u) : 4u * (uint32_t)nsm;
-  k_base_primes<<<grid, kBaseThreads, 0, s>>>(r, rs, primes, recips, cap, nbase, flags, epoch);
+  k_base_primes<<<grid, kBaseThreads, 0, s>>>(r, rs, primes, recips, cap, nbase, flags, epoch, prof);
   return cudaGetLastError();
 }
 

@@ -313,7 +313,7 @@ int base_primes(uint64_t r, uint32_t *primes, uint64_t *recips, uint64_t cap, ui
     g.epoch = 1;
   }
   CUDA_TRY(sv::launch_base_primes((uint32_t)r, rs, primes, recips, (uint32_t)cap, nbase,
-                                  g.kflags.p ? g.kflags.p : nullptr, g.epoch, g.nsm, s));
+                                  g.kflags.p ? g.kflags.p : nullptr, g.epoch, g.nsm, g.prof, s));
   g_launches += 1;
   return 0;
 }

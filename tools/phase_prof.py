@@ -10,7 +10,7 @@ for spec in sys.argv[1:] or [""]:
     kw = {k: int(v) for k, v in kw.items()}
     sv.set_options(**kw)
     sv.stats(lo, hi)
-    c = torch.zeros(112, dtype=torch.int64, device="cuda")
+    c = torch.zeros(120, dtype=torch.int64, device="cuda")
     sv.debug_set_profile(c)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(); ev0.record(); r = sv.stats(lo, hi); ev1.record(); torch.cuda.synchronize()

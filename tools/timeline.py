@@ -16,7 +16,7 @@ for spec in sys.argv[1:]:
     sv.base_primes_async(r, b.primes, b.recips, b.nbase)
     rows = []
     for i in range(8):
-        c = torch.zeros(112, dtype=torch.int64, device="cuda")
+        c = torch.zeros(120, dtype=torch.int64, device="cuda")
         sv.debug_set_profile(c)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(); sv.stats_async(lo, hi, b.primes, b.recips, b.nbase, res); e1.record()
