@@ -4,10 +4,12 @@ configs[2], "config 3"), count + prime sum, on 1/2/4/8 B200 (one process per
 GPU under torchrun).
 
 One step = one pass of the whole hot path:
-  A2 base primes (K1; every rank, or rank 0 + A9 NCCL broadcast with
-  --broadcast) -> A3-A6 segmented sieve of the rank's block (count + sum) ->
-  A9 all-reduce (N>1): by default inside the sieve kernel's last CTA over
-  NVLink peer memory (F4, csrc/peer.cuh), `--allreduce nccl` for NCCL.
+  A2 base primes -> A3-A6 segmented sieve of the rank's block (count + sum)
+  -> A9 all-reduce (N>1).  By default ONE kernel launch per rank does all of
+  it: the base primes of the rank's block are computed inside the sieve
+  kernel (fused A2, cooperative launch), and the all-reduce runs in its last
+  CTA over NVLink peer memory (F4, csrc/peer.cuh).  --broadcast: K1 on rank 0
+  + NCCL broadcast instead; --allreduce nccl: a separate NCCL all-reduce.
 
 Timing: W untimed warm-up steps; then K steps bracketed by barrier +
 synchronize on both sides; every step is timed with CUDA events on the
@@ -269,15 +271,18 @@ def main():
     def step(e=None):
         with torch.cuda.stream(stream):
             if e: e[0].record(stream)
-            if rank == 0 or not bcast:
-                sv.base_primes_async(r, base.primes, base.recips, base.nbase)
-            if bcast:
+            if bcast:  # A2 on rank 0 + A9 NCCL broadcast, then the sieve
+                if rank == 0:
+                    sv.base_primes_async(r, base.primes, base.recips, base.nbase)
                 tdist.broadcast(base.packed, src=0)
-            if e: e[1].record(stream)
-            if fused:  # sieve + all-reduce in one kernel
-                sv.stats_allreduce_async(a, b, base.primes, base.recips, base.nbase, result)
-            else:
-                sv.stats_async(a, b, base.primes, base.recips, base.nbase, result)
+                if e: e[1].record(stream)
+                if fused:
+                    sv.stats_allreduce_async(a, b, base.primes, base.recips, base.nbase, result)
+                else:
+                    sv.stats_async(a, b, base.primes, base.recips, base.nbase, result)
+            else:  # A2 + A3..A7 (+ the fused all-reduce) in one launch
+                if e: e[1].record(stream)
+                sv.stats_base_async(a, b, base.primes, base.recips, base.nbase, result, fused)
             if e: e[2].record(stream)
             if world > 1 and not fused:
                 tdist.all_reduce(result, op=tdist.ReduceOp.SUM)
@@ -352,13 +357,16 @@ def main():
         clocks = sampler.summary()
         peaks = load_peaks()
         sm_max = peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0
-        m_alg = algorithmic_marks(a, b)  # rank 0's block (the whole range at N=1)
+        # whole-job marks / max-over-ranks kernel time, against
+        # N x the per-GPU peak (at N=1: the one launch)
+        m_alg = algorithmic_marks(lo, hi)
         achieved = m_alg / (sieve_ms_mean / 1e3) / 1e9
-        peak = 148 * SMEM_LANES_PER_CLK * sm_max * 1e6 / 1e9
+        peak = world * 148 * SMEM_LANES_PER_CLK * sm_max * 1e6 / 1e9
         roof = {"bound": "smem_atomic", "achieved": achieved, "peak": peak, "unit": "Gmarks/s",
                 "frac": achieved / peak, "traffic": load_traffic(),
-                "kernel": "sv::k_sieve<NG,kCount>", "marks_alg_per_launch": m_alg,
-                "peak_basis": f"148 SMs x {SMEM_LANES_PER_CLK} shared-memory lanes/clk x "
+                "kernel": "sv::k_sieve<NG,kCount>" + ("" if bcast else " (A2 fused)"),
+                "marks_alg_per_launch": algorithmic_marks(a, b), "marks_alg_job": m_alg,
+                "peak_basis": f"{world} x 148 SMs x {SMEM_LANES_PER_CLK} shared-memory lanes/clk x "
                               f"{sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
                 "kernel_ms": sieve_ms_mean, "kernel_share_of_step": sieve_ms_mean / ms_per_step}
         out = {
@@ -367,7 +375,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "config3: pi(1e10) count + prime sum over [2, 1e10+1)",
                        "lo": lo, "hi": hi, "segment_kb": opts["segment_kb"], "wheel": opts["wheel"],
-                       "threads": opts["threads"], "base_primes": "broadcast" if bcast else "per-rank",
+                       "threads": opts["threads"], "base_primes": "rank 0 + NCCL broadcast" if bcast else "per rank, fused into the sieve launch",
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
                        "parallelism": f"range split over {world} GPU(s)",
                        "allreduce": ("none" if world == 1 else

@@ -132,6 +132,18 @@ int sieve_prepare_base_async(const uint32_t *primes, const uint32_t *nbase, uint
 int sieve_stats_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const uint64_t *recips,
                       const uint32_t *nbase, uint64_t *result);
 
+/* Steps A2 + A3..A7 in ONE launch: the base primes <= isqrt(hi-1) are
+ * computed into primes/recips/nbase (as sieve_base_primes_async would; cap
+ * >= sieve_base_capacity(isqrt(hi-1))) by the sieve kernel itself -- every
+ * CTA sieves a slice of the odd numbers <= r, two grid barriers of a
+ * cooperative launch order them -- and then result[0..1] = (count, sum mod
+ * 2^64) of [lo, hi).  allreduce != 0: the result is summed over the attached
+ * peers as in sieve_stats_allreduce_async.  When a CTA's slice would not fit
+ * its shared-memory segment (huge r, tiny range) the library runs the
+ * base-prime kernel first instead; the results are the same. */
+int sieve_stats_base_async(uint64_t lo, uint64_t hi, uint32_t *primes, uint64_t *recips,
+                           uint32_t *nbase, uint64_t cap, int allreduce, uint64_t *result);
+
 /* Bitmap mode: writes sieve_bitmap_words(lo,hi) words into out (device,
  * 16-byte aligned for vector stores; any alignment accepted) and
  * result[0..1] as above. */
@@ -207,7 +219,9 @@ uint64_t sieve_kernel_launches(void);
  * entry, [105] max entry, [106] max end of prologue, [107] max end of
  * sieving, [108] result written, [109] ~min end of sieving; of the base-
  * prime kernel: [112] ~min entry, [113] small primes, [114] slice marked,
- * [115] list offset known, [116] end (max over CTAs).  The buffer must hold
+ * [115] list offset known, [116] end (max over CTAs); of the fused A2 phase:
+ * [110] slice counted, [111] barrier 1 passed, [117] primes written, [118]
+ * barrier 2 passed.  The buffer must hold
  * 120 entries.  NULL disables (the default). */
 int sieve_debug_set_profile(uint64_t *dev_counters);
 

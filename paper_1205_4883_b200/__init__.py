@@ -42,6 +42,7 @@ from ._abi import (  # noqa: F401
     stats,
     stats_allreduce_async,
     stats_async,
+    stats_base_async,
 )
 
 __all__ = [
@@ -50,5 +51,5 @@ __all__ = [
     "set_device", "set_stream", "get_stream", "set_options", "get_options", "shutdown",
     "kernel_launches", "lib", "library_path", "modpow", "fermat", "is_prime",
     "peer_slab_handle", "peer_attach", "peer_attach_ptrs", "peer_detach", "peer_epoch",
-    "stats_allreduce_async", "IPC_HANDLE_BYTES", "MAX_PEERS", "PEER_SLAB_BYTES",
+    "stats_allreduce_async", "stats_base_async", "IPC_HANDLE_BYTES", "MAX_PEERS", "PEER_SLAB_BYTES",
 ]

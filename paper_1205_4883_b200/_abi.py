@@ -78,6 +78,7 @@ def lib():
             "sieve_peer_detach": (ctypes.c_int, []),
             "sieve_peer_epoch": (_u64, []),
             "sieve_stats_allreduce_async": (ctypes.c_int, [_u64, _u64, _p, _p, _p, _p]),
+            "sieve_stats_base_async": (ctypes.c_int, [_u64, _u64, _p, _p, _p, _u64, ctypes.c_int, _p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -169,6 +170,14 @@ def prepare_base_async(primes_t, nbase_t, recips_t) -> None:
 def stats_async(lo: int, hi: int, primes_t, recips_t, nbase_t, result_t) -> None:
     _check(lib().sieve_stats_async(lo, hi, _ptr(primes_t), _ptr(recips_t), _ptr(nbase_t),
                                    _ptr(result_t)))
+
+
+def stats_base_async(lo: int, hi: int, primes_t, recips_t, nbase_t, result_t,
+                     allreduce: bool = False) -> None:
+    """Base primes (into primes_t/recips_t/nbase_t) and count/sum of [lo, hi)
+    in one kernel launch (fused A2); allreduce: summed over attached peers."""
+    _check(lib().sieve_stats_base_async(lo, hi, _ptr(primes_t), _ptr(recips_t), _ptr(nbase_t),
+                                        primes_t.numel(), 1 if allreduce else 0, _ptr(result_t)))
 
 
 def bitmap_async(lo: int, hi: int, primes_t, recips_t, nbase_t, out_t, result_t) -> None:

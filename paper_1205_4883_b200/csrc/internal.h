@@ -155,6 +155,17 @@ struct SieveParams {
   uint64_t pepoch;
   uint64_t timeout_ns;
   uint32_t world, rank;
+  // fused A2 (count/bitmap/list; bprimes == nullptr: off): before sieving,
+  // CTA c computes the odd primes of slice c of the odd numbers <= r into
+  // bprimes/brecips (the buffers primes/recips point to) and *bnbase, with
+  // two grid barriers (cooperative launch: all CTAs resident).
+  uint32_t *bprimes;
+  uint64_t *brecips;
+  uint32_t *bnbase;
+  uint32_t bcap;        // capacity of bprimes/brecips
+  uint32_t rs;          // isqrt(r)
+  uint32_t *bcounts;    // [gridDim.x] per-CTA prime counts
+  unsigned int *gbar;   // grid barrier counter: 0 at launch, reset by the last CTA
 };
 
 // Diagnostic flag: skip step A4/A5 (wheel init + count/write-back only), to
@@ -166,6 +177,9 @@ constexpr uint32_t kFlagSkipMarking = 1u;
 constexpr uint32_t kFlagSkipA = 2u, kFlagSkipB = 4u, kFlagSkipC = 8u;
 
 enum Mode { kCount = 0, kBitmap = 1, kBatch = 2, kList = 3 };
+
+// fused A2 scratch in the segment buffer: small primes (words) + staging
+constexpr uint64_t kMaxSmallWords = 1024;
 
 // launchers (kernels.cu)
 cudaError_t launch_sieve(int ng, int mode, const SieveParams &p, int grid, int threads,

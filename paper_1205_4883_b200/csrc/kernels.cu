@@ -59,13 +59,18 @@ __device__ __forceinline__ uint32_t first_hit(uint64_t a, uint64_t seg_end, uint
 // T = (2^64-1) - q p (|T| < 2^40, so mod-2^64 arithmetic gives it as a signed
 // number) corrects q by floor(T / p), with a final +-1 guard on the rounding.
 __device__ __forceinline__ uint64_t recip_of(uint32_t p) {
-  uint64_t q = __double2ull_rz(1.8446744073709552e19 / (double)p);
+  // floor((2^64 - 1) / p), p >= 3: a double estimate q (within ~2^12 of the
+  // quotient: one reciprocal, no division), then exact integer correction
+  // of the remainder T = (2^64 - 1) - q p (|T| < 2^45: read as signed)
+  const double r = __drcp_rn((double)p);
+  uint64_t q = __double2ull_rz(1.8446744073709552e19 * r);
   int64_t T = (int64_t)(~0ull - q * (uint64_t)p);
-  int64_t d = (int64_t)floor((double)T / (double)p);
+  const int64_t d = (int64_t)floor((double)T * r);
+  q += (uint64_t)d;
   T -= d * (int64_t)p;
-  if (T < 0) { --d; T += p; }
-  if (T >= (int64_t)p) ++d;
-  return q + (uint64_t)d;
+  while (T < 0) { --q; T += p; }
+  while (T >= (int64_t)p) { ++q; T -= p; }
+  return q;
 }
 
 __device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t *v, uint32_t n, uint64_t x) {
@@ -745,6 +750,103 @@ __device__ __forceinline__ void block_sum2(unsigned long long &x, unsigned long 
   }
 }
 
+// ---------------------------------------------------------------------------
+// A2 building blocks shared by the base-prime kernel K1 and its fused form
+// in the sieve kernel (base_phase): odd n = 2i + 1, bit b of a word <-> i = I + b.
+// ---------------------------------------------------------------------------
+constexpr int kNumPat = 10;  // pattern primes 3..31
+constexpr uint32_t kMaxSmall = 1024;  // odd primes <= 4096 number 563
+// bits (q - 3) / 2 of the odd numbers from 3 (i = 1 at bit 0): the pattern
+// primes themselves, and (kSelfMini) also the mini-sieve primes 37..61
+constexpr uint32_t kSelfPat = (1u << 0) | (1u << 1) | (1u << 2) | (1u << 4) | (1u << 5) |
+                              (1u << 7) | (1u << 8) | (1u << 10) | (1u << 13) | (1u << 14);
+constexpr uint32_t kSelfMini = kSelfPat | (1u << 17) | (1u << 19) | (1u << 20) | (1u << 22) |
+                               (1u << 25) | (1u << 28) | (1u << 29);
+
+// bit b of the result is set iff 2(I + b) + 1 is an odd multiple of a pattern
+// prime 3..31: for q, the bits b = ((q-1)/2 - I) mod q + k q
+__device__ __forceinline__ uint32_t pattern_word(uint32_t I) {
+  constexpr uint32_t kQ[kNumPat] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31};
+  uint32_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kNumPat; ++k) {
+    const uint32_t q = kQ[k], h = (q - 1u) / 2u;
+    uint32_t pat = 0;  // bits 0, q, 2q, ... < 32 (constant-folded)
+    for (uint32_t b = 0; b < 32u; b += q) pat |= 1u << b;
+    const uint32_t t = I % q;
+    const uint32_t f = h >= t ? h - t : h + q - t;
+    v |= pat << f;
+  }
+  return v;
+}
+
+// The odd primes 3 <= q <= rs (rs <= 4096), ascending, into sp[]: a
+// mini-sieve of i = 1..2047 by the primes <= 61 (warps 0 and 1, one word per
+// thread) and an ordered compaction.  Called by the whole CTA (>= 64
+// threads); stage needs 128 words; returns the count (all threads).
+__device__ __forceinline__ uint32_t small_primes(uint32_t rs, uint32_t *sp, uint32_t *stage,
+                                                 uint32_t *s_w2) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (warp < 2u) {
+    const uint32_t I = 1u + 32u * tid;  // first i of word tid
+    uint32_t v = pattern_word(I);
+    constexpr uint32_t big[7] = {37, 41, 43, 47, 53, 59, 61};  // at most one multiple per word
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      const uint32_t q = big[k], h = (q - 1u) / 2u, t = I % q;
+      const uint32_t f = h >= t ? h - t : h + q - t;
+      if (f < 32u) v |= 1u << f;
+    }
+    if (tid == 0) v &= ~kSelfMini;
+    uint32_t x = ~v;
+    const uint32_t imax_s = rs >= 3u ? (rs - 1u) / 2u : 0u;  // keep n = 2i + 1 <= rs
+    if (I > imax_s) x = 0;
+    else if (imax_s - I < 31u) x &= (2u << (imax_s - I)) - 1u;
+    const uint32_t c = __popc(x);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane == 31u) s_w2[warp] = incl;
+    stage[tid] = x;
+    stage[64u + tid] = incl - c;
+  }
+  __syncthreads();
+  if (warp < 2u) {
+    uint32_t x = stage[tid], o = stage[64u + tid] + (warp ? s_w2[0] : 0u);
+    while (x) {
+      const uint32_t b = __ffs(x) - 1u;
+      x &= x - 1u;
+      if (o < kMaxSmall) sp[o] = 2u * (1u + 32u * tid + b) + 1u;
+      ++o;
+    }
+  }
+  __syncthreads();
+  return min(s_w2[0] + s_w2[1], kMaxSmall);
+}
+
+// Mark the odd multiples >= q^2 of the small primes q = sp[m31..nsp) > 31 in
+// the slice bitmap bm (bit j <-> odd a + 2j, nbits bits): one warp per prime,
+// lanes on consecutive hits.  sp ascending: per warp, q^2 >= e ends the loop.
+__device__ __forceinline__ void mark_slice(uint32_t *bm, const uint32_t *sp, uint32_t m31,
+                                           uint32_t nsp, uint32_t a, uint32_t nbits) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t e = a + 2u * nbits;
+  for (uint32_t m = m31 + warp; m < nsp; m += nw) {
+    const uint32_t q = sp[m];
+    uint32_t f = q * q;
+    if (f >= e) break;
+    if (f < a) {
+      f = ((a + q - 1u) / q) * q;
+      if (!(f & 1u)) f += q;
+    }
+    for (uint32_t j = (f - a) / 2u + lane * q; j < nbits; j += 32u * q)
+      atomicOr(&bm[j >> 5], 1u << (j & 31));
+  }
+}
+
 // First index with v[idx] > x, by one warp: 32-ary search (each round the
 // 32 lanes sample 32 evenly spaced entries; a ballot of "<= x" narrows the
 // interval 32-fold), so a search over 2^18 primes costs ~4 dependent loads.
@@ -794,6 +896,136 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
   }
 }
 
+// Grid-wide barrier of a cooperative launch: thread 0 of each CTA arrives
+// on *bar and waits for `target` arrivals (the counter only grows within a
+// launch: the n-th barrier waits for n * gridDim.x).
+__device__ __forceinline__ void grid_barrier(unsigned int *bar, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned int v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+// Fused A2 (the base-prime kernel's work inside the sieve kernel, before the
+// first segment): CTA c sieves slice c of the odd numbers 3..r (L bits,
+// L = ceil(imax / G) rounded up to 32; the host checks that the small
+// primes, the slice bitmap and its staged primes fit in the segment buffer
+// below the wheel tables, used here as scratch), counts its
+// primes and publishes the count; after a grid barrier it places them by the
+// counts of the slices before it and writes primes and reciprocals; a second
+// grid barrier makes the whole list visible before any CTA reads it.
+__device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) {
+  __shared__ uint32_t s_w[32];
+  __shared__ unsigned long long s_base;  // this slice's first list index
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x >> 5;
+  const uint32_t G = gridDim.x;
+  uint32_t *sp = seg;                   // [kMaxSmall]
+  uint32_t *bm = seg + kMaxSmall + 128u;  // slice bitmap
+  const uint32_t nsp = small_primes(P.rs, sp, seg + kMaxSmall, s_w);
+  const uint32_t m31 = min(nsp, (uint32_t)kNumPat);
+  const uint32_t imax = P.r >= 3u ? (P.r - 1u) / 2u : 0u;
+  const uint32_t L = ((imax + G - 1u) / G + 31u) & ~31u;
+  const uint32_t i0 = 1u + blockIdx.x * L;
+  const uint32_t nbits = i0 <= imax ? min(L, imax - i0 + 1u) : 0u;
+  const uint32_t nwd = (nbits + 31u) >> 5;
+  const uint32_t a = 2u * i0 + 1u;
+  for (uint32_t w = tid; w < nwd; w += blockDim.x) {
+    uint32_t v = pattern_word(i0 + 32u * w);
+    if (blockIdx.x == 0 && w == 0) v &= ~kSelfPat;  // 3..31 are prime
+    bm[w] = v;
+  }
+  __syncthreads();
+  mark_slice(bm, sp, m31, nsp, a, nbits);
+  __syncthreads();
+  // survivors of word w (primes = clear bits below nbits)
+  auto word = [&](uint32_t w) {
+    uint32_t x = ~bm[w];
+    const uint32_t vb = nbits - 32u * w;
+    if (vb < 32u) x &= (1u << vb) - 1u;
+    return x;
+  };
+  uint32_t c = 0;
+  for (uint32_t w = tid; w < nwd; w += blockDim.x) c += __popc(word(w));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) s_w[warp] = c;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t t = 0;
+    for (uint32_t k = 0; k < nw; ++k) t += s_w[k];
+    P.bcounts[blockIdx.x] = t;
+    if (P.prof) atomicMax(P.prof + 110, global_ns());
+  }
+  grid_barrier(P.gbar, G);
+  if (P.prof && tid == 0) atomicMax(P.prof + 111, global_ns());
+  if (warp == 0) {  // this slice's offset and the total
+    unsigned long long before = 0, all = 0;
+    for (uint32_t k = lane; k < G; k += 32u) {
+      const unsigned long long v = __ldcg(P.bcounts + k);
+      all += v;
+      if (k < blockIdx.x) before += v;
+    }
+    before = warp_sum_u64(before);
+    all = warp_sum_u64(all);
+    if (lane == 0) {
+      s_base = before;
+      if (blockIdx.x == 0) *P.bnbase = (uint32_t)min(all, (unsigned long long)P.bcap);
+    }
+  }
+  __syncthreads();
+  // ordered emission: the slice's primes staged in shared memory by a block
+  // scan per row of blockDim.x words, then one prime (and its reciprocal)
+  // per thread, coalesced
+  uint32_t *stage = bm + nwd;  // <= nbits / 3 + 2 entries (host-checked space)
+  uint32_t o = 0;
+  for (uint32_t w0 = 0; w0 < nwd; w0 += blockDim.x) {
+    const uint32_t w = w0 + tid;
+    uint32_t x = w < nwd ? word(w) : 0u;
+    const uint32_t cw = __popc(x);
+    uint32_t incl = cw;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= (uint32_t)d) incl += y;
+    }
+    __syncthreads();  // s_w reuse
+    if (lane == 31u) s_w[warp] = incl;
+    __syncthreads();
+    uint32_t excl = incl - cw, row = 0;
+    for (uint32_t k = 0; k < nw; ++k) {
+      if (k < warp) excl += s_w[k];
+      row += s_w[k];
+    }
+    uint32_t q = o + excl;
+    while (x) {
+      const uint32_t b = __ffs(x) - 1u;
+      x &= x - 1u;
+      stage[q++] = a + 2u * (32u * w + b);
+    }
+    o += row;
+  }
+  __syncthreads();
+  const unsigned long long base = s_base;
+  for (uint32_t t = tid; t < o; t += blockDim.x) {
+    if (base + t < P.bcap) {
+      const uint32_t p = stage[t];
+      P.bprimes[base + t] = p;
+      P.brecips[base + t] = recip_of(p);
+    }
+  }
+  if (P.prof && tid == 0) atomicMax(P.prof + 117, global_ns());
+  grid_barrier(P.gbar, 2u * G);
+  if (P.prof && tid == 0) atomicMax(P.prof + 118, global_ns());
+}
+
 // ---------------------------------------------------------------------------
 // The segmented sieve kernel.  Persistent CTAs walk the segments round robin;
 // each segment lives in shared memory for its whole life (init -> mark ->
@@ -823,6 +1055,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     atomicMax(P.prof + 105, t);
   }
   for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
+  if (MODE != kBatch && P.bprimes) base_phase(P, seg);  // fused A2 (scratch below tab)
   compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
   __syncthreads();
   if (P.prof && threadIdx.x == 0) atomicMax(P.prof + 106, global_ns());
@@ -941,6 +1174,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       P.result[0] = c;
       P.result[1] = sm;
       *P.done = 0u;  // ready for the next launch
+      if (P.gbar) *P.gbar = 0u;  // every CTA is past both grid barriers
       if (P.prof) atomicMax(P.prof + 108, global_ns());
     }
   }
@@ -969,31 +1203,11 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
 // ---------------------------------------------------------------------------
 constexpr uint32_t kBaseThreads = 256;
 constexpr uint32_t kSliceBits = 32u * kBaseThreads;  // one word per thread
-constexpr uint32_t kMaxSmall = 1024;                 // odd primes <= 4096 number 563
-constexpr uint32_t kMaxSlicePrimes = 2048;           // primes among 8192 odd n: <= 1899 (slice 0)
-constexpr int kNumPat = 10;                          // pattern primes 3..31
-
 __device__ __forceinline__ uint64_t make_flag(uint32_t epoch, uint64_t v, uint64_t st) {
   return ((uint64_t)epoch << 48) | (v << 2) | st;
 }
 
-// bit b of the result is set iff 2(I + b) + 1 is an odd multiple of a pattern
-// prime 3..31: for q, the bits b = ((q-1)/2 - I) mod q + k q
-__device__ __forceinline__ uint32_t pattern_word(uint32_t I) {
-  constexpr uint32_t kQ[kNumPat] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31};
-  uint32_t v = 0;
-#pragma unroll
-  for (int k = 0; k < kNumPat; ++k) {
-    const uint32_t q = kQ[k], h = (q - 1u) / 2u;
-    uint32_t pat = 0;  // bits 0, q, 2q, ... < 32 (constant-folded)
-    for (uint32_t b = 0; b < 32u; b += q) pat |= 1u << b;
-    const uint32_t t = I % q;
-    const uint32_t f = h >= t ? h - t : h + q - t;
-    v |= pat << f;
-  }
-  return v;
-}
-
+constexpr uint32_t kMaxSlicePrimes = 2048;           // primes among 8192 odd n: <= 1899 (slice 0)
 __global__ void __launch_bounds__(kBaseThreads) k_base_primes(uint32_t r, uint32_t rs, uint32_t *primes,
                                                               uint64_t *recips, uint32_t cap,
                                                               uint32_t *nbase, uint64_t *flags,
@@ -1002,7 +1216,6 @@ __global__ void __launch_bounds__(kBaseThreads) k_base_primes(uint32_t r, uint32
   __shared__ uint32_t sp[kMaxSmall];
   __shared__ uint32_t s_list[kMaxSlicePrimes];
   __shared__ uint32_t s_w[kBaseThreads / 32];
-  __shared__ uint32_t s_nsp;
   __shared__ unsigned long long s_off;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nw = blockDim.x >> 5;
   // diagnostics timeline (prof[112..116], globaltimer ns; min as max of ~t)
@@ -1011,52 +1224,8 @@ __global__ void __launch_bounds__(kBaseThreads) k_base_primes(uint32_t r, uint32
   };
   stamp(112);
 
-  // odd primes 3 <= q <= rs (rs <= 4096): mini-sieve of i = 1..2047 (n = 2i+1)
-  // by the primes <= 61, then an ordered compaction (two warps)
-  if (warp < 2u) {
-    const uint32_t I = 1u + 32u * tid;  // first i of word tid
-    uint32_t v = pattern_word(I);
-    constexpr uint32_t big[7] = {37, 41, 43, 47, 53, 59, 61};  // at most one multiple per word
-#pragma unroll
-    for (int k = 0; k < 7; ++k) {
-      const uint32_t q = big[k], h = (q - 1u) / 2u, t = I % q;
-      const uint32_t f = h >= t ? h - t : h + q - t;
-      if (f < 32u) v |= 1u << f;
-    }
-    if (tid == 0) {  // the sieving primes themselves: i = (q-1)/2, bit i - 1
-      v &= ~((1u << 0) | (1u << 1) | (1u << 2) | (1u << 4) | (1u << 5) | (1u << 7) | (1u << 8) |
-             (1u << 10) | (1u << 13) | (1u << 14) | (1u << 17) | (1u << 19) | (1u << 20) |
-             (1u << 22) | (1u << 25) | (1u << 28) | (1u << 29));
-    }
-    uint32_t x = ~v;
-    // keep n = 2i + 1 <= rs: i <= (rs - 1) / 2
-    const uint32_t imax_s = rs >= 3u ? (rs - 1u) / 2u : 0u;
-    if (I > imax_s) x = 0;
-    else if (imax_s - I < 31u) x &= (2u << (imax_s - I)) - 1u;
-    const uint32_t c = __popc(x);
-    uint32_t incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= (uint32_t)o) incl += y;
-    }
-    if (lane == 31u) s_w[warp] = incl;
-    bm[tid] = x;  // staged: the compaction needs warp 0's total
-    bm[64u + tid] = incl - c;
-  }
-  __syncthreads();
-  if (warp < 2u) {
-    uint32_t x = bm[tid], o = bm[64u + tid] + (warp ? s_w[0] : 0u);
-    while (x) {
-      const uint32_t b = __ffs(x) - 1u;
-      x &= x - 1u;
-      if (o < kMaxSmall) sp[o] = 2u * (1u + 32u * tid + b) + 1u;
-      ++o;
-    }
-    if (tid == 0) s_nsp = s_w[0] + s_w[1];
-  }
-  __syncthreads();
-  const uint32_t nsp = min(s_nsp, kMaxSmall);
+  // odd primes 3 <= q <= rs (rs <= 4096), ascending
+  const uint32_t nsp = small_primes(rs, sp, bm, s_w);
   // first index with sp > 31 (sp holds 3, 5, ..., 31 first when rs >= 31)
   const uint32_t m31 = min(nsp, (uint32_t)kNumPat);
   stamp(113);
@@ -1066,26 +1235,12 @@ __global__ void __launch_bounds__(kBaseThreads) k_base_primes(uint32_t r, uint32
   for (uint32_t k = blockIdx.x; k < nslice; k += gridDim.x) {
     const uint32_t i0 = 1 + k * kSliceBits;
     const uint32_t nbits = min(kSliceBits, imax - i0 + 1);
-    const uint32_t a = 2u * i0 + 1u, e = a + 2u * nbits;  // odd integers [a, e)
+    const uint32_t a = 2u * i0 + 1u;  // odd integers [a, a + 2 nbits)
     uint32_t v = pattern_word(i0 + 32u * tid);
-    if (k == 0 && tid == 0) {  // 3..31 are prime: bits (q - 3) / 2
-      v &= ~((1u << 0) | (1u << 1) | (1u << 2) | (1u << 4) | (1u << 5) | (1u << 7) | (1u << 8) |
-             (1u << 10) | (1u << 13) | (1u << 14));
-    }
+    if (k == 0 && tid == 0) v &= ~kSelfPat;  // 3..31 are prime
     bm[tid] = v;
     __syncthreads();
-    // one warp per prime q > 31 (ascending per warp: past q^2 >= e, stop)
-    for (uint32_t m = m31 + warp; m < nsp; m += nw) {
-      const uint32_t q = sp[m];
-      uint32_t f = q * q;
-      if (f >= e) break;
-      if (f < a) {
-        f = ((a + q - 1u) / q) * q;
-        if (!(f & 1u)) f += q;
-      }
-      for (uint32_t j = (f - a) / 2u + lane * q; j < nbits; j += 32u * q)
-        atomicOr(&bm[j >> 5], 1u << (j & 31));
-    }
+    mark_slice(bm, sp, m31, nsp, a, nbits);
     __syncthreads();
     stamp(114);
     uint32_t x = ~bm[tid];
@@ -1170,6 +1325,19 @@ __global__ void k_item_ends(BatchItem *items, uint64_t n, const uint32_t *__rest
 // ---------------------------------------------------------------------------
 template <int NG, int MODE>
 static cudaError_t launch_t(const SieveParams &p, int grid, int threads, size_t smem, cudaStream_t s) {
+  if (p.bprimes) {  // fused A2: grid barriers need every CTA resident
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_sieve<NG, MODE>, p);
+  }
   k_sieve<NG, MODE><<<grid, threads, smem, s>>>(p);
   return cudaGetLastError();
 }

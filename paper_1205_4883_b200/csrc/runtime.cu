@@ -129,6 +129,8 @@ struct Ctx {
   DevBuf<uint2> buckets;  // step A5 bucket rings
   DevBuf<uint64_t> kflags;  // K1 look-back flags (epoch-tagged, never reset)
   uint32_t epoch = 0;
+  DevBuf<uint32_t> bcounts;    // fused A2: per-CTA prime counts
+  DevBuf<unsigned int> gbar;   // fused A2: grid barrier counter (kept 0 between launches)
   DevBuf<unsigned long long> lflags;  // list-mode look-back flags (epoch-tagged)
   uint32_t lepoch = 0;
   uint64_t *h_res = nullptr;  // pinned [2]
@@ -370,9 +372,53 @@ int setup_buckets(sv::SieveParams &sp, int grid) {
   return 0;
 }
 
-int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork) {
+// Where a sieve launch gets its base primes (A2): already in sp.primes
+// (req == nullptr), or computed into req's buffers in the same launch (fused
+// A2, cooperative) when every CTA's slice of the odd numbers <= r fits its
+// segment buffer, else by K1 first.
+struct BaseReq {
+  uint32_t *primes;
+  uint64_t *recips;
+  uint32_t *nbase;
+  uint64_t cap;
+  uint64_t r;
+};
+
+// scratch of the fused A2 in the segment buffer (S bits, below the wheel
+// tables): small primes and staging, the slice bitmap (L bits) and its
+// primes staged for emission (<= L/3 + 2: one of three consecutive odd
+// numbers is a multiple of 3)
+bool fused_fits(uint64_t r, int grid, uint64_t sbits) {
+  if (g.opt.ctas_per_sm > 0 && (int)g.opt.ctas_per_sm > g.occ) return false;  // not co-resident
+  const uint64_t imax = r >= 3 ? (r - 1) / 2 : 0;
+  const uint64_t L = ((imax + grid - 1) / grid + 31) / 32 * 32;
+  return sv::kMaxSmallWords + 128 + L / 32 + L / 3 + 2 <= sbits / 32;
+}
+
+int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork, const BaseReq *req = nullptr) {
   TRY(ensure_smem_attr());
   const int grid = grid_for(nwork);
+  if (req) {
+    if (fused_fits(req->r, grid, sp.seg_bits)) {
+      if (!g.gbar.p) {
+        TRY(g.gbar.ensure(1));
+        CUDA_TRY(cudaMemsetAsync(g.gbar.p, 0, sizeof(unsigned int), g.stream()));
+      }
+      TRY(g.bcounts.ensure((size_t)grid));
+      sp.bprimes = req->primes;
+      sp.brecips = req->recips;
+      sp.bnbase = req->nbase;
+      sp.bcap = (uint32_t)std::min<uint64_t>(req->cap, 0xFFFFFFFFull);
+      sp.rs = (uint32_t)isqrt_u64(req->r);
+      sp.bcounts = g.bcounts.p;
+      sp.gbar = g.gbar.p;
+    } else {
+      TRY(base_primes(req->r, req->primes, req->recips, req->cap, req->nbase, g.stream()));
+    }
+    sp.primes = req->primes;
+    sp.recips = req->recips;
+    sp.nbase = req->nbase;
+  }
   TRY(g.partials.ensure(2 * (size_t)grid));
   sp.partials = g.partials.p;
   // not in list mode: its look-back needs the segments of a wave in flight
@@ -386,34 +432,46 @@ int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork) {
 
 // count/sum of [lo, hi) into device result[0..1]; empty/odd-free ranges handled
 int stats_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase,
-                uint64_t *result) {
+                uint64_t *result, const BaseReq *req = nullptr) {
   if (P.nbits == 0) {
+    if (req) TRY(base_primes(req->r, req->primes, req->recips, req->cap, req->nbase, g.stream()));
     uint64_t h[2] = {P.two ? 1ull : 0ull, P.two ? 2ull : 0ull};
     CUDA_TRY(cudaMemcpyAsync(result, h, sizeof h, cudaMemcpyHostToDevice, g.stream()));
     CUDA_TRY(cudaStreamSynchronize(g.stream()));  // h is on this stack frame
     return 0;
   }
   sv::SieveParams sp = params_for(P, primes, recips, nbase, result);
-  return run_sieve(sv::kCount, sp, P.nseg);
+  return run_sieve(sv::kCount, sp, P.nseg, req);
 }
 
 int bitmap_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase,
-                 uint32_t *out, uint64_t *result) {
-  if (P.nbits == 0) return stats_async(P, primes, recips, nbase, result);
+                 uint32_t *out, uint64_t *result, const BaseReq *req = nullptr) {
+  if (P.nbits == 0) return stats_async(P, primes, recips, nbase, result, req);
   sv::SieveParams sp = params_for(P, primes, recips, nbase, result);
   sp.out = out;
   sp.out_words = P.words;
   sp.out_vec4 = ((uintptr_t)out & 15u) == 0 ? 1u : 0u;
-  return run_sieve(sv::kBitmap, sp, P.nseg);
+  return run_sieve(sv::kBitmap, sp, P.nseg, req);
+}
+
+// the library's own base-prime buffers, sized for r, as a fused-A2 request
+int own_req(uint64_t r, BaseReq &q) {
+  const uint64_t cap = base_capacity(r);
+  TRY(g.primes.ensure(cap));
+  TRY(g.recips.ensure(cap));
+  TRY(g.nbase.ensure(1));
+  q = BaseReq{g.primes.p, g.recips.p, g.nbase.p, cap, r};
+  return 0;
 }
 
 // F4: count/sum of this rank's [lo, hi) summed over every attached rank, the
 // all-reduce done inside the sieve kernel's last CTA (peer.cuh)
 int stats_allreduce_async(const Plan &P, const uint32_t *primes, const uint64_t *recips,
-                          const uint32_t *nbase, uint64_t *result) {
+                          const uint32_t *nbase, uint64_t *result, const BaseReq *req = nullptr) {
   auto &pe = g.peer;
   pe.epoch += 1;
   if (P.nbits == 0) {  // no sieve launch: publish (0, 0) or (1, 2) alone
+    if (req) TRY(base_primes(req->r, req->primes, req->recips, req->cap, req->nbase, g.stream()));
     CUDA_TRY(sv::launch_peer_only(pe.ptrs.p, pe.world, pe.rank, pe.epoch, pe.timeout_ns,
                                   P.two ? 1 : 0, P.two ? 2 : 0, result, g.stream()));
     g_launches += 1;
@@ -425,7 +483,7 @@ int stats_allreduce_async(const Plan &P, const uint32_t *primes, const uint64_t 
   sp.timeout_ns = pe.timeout_ns;
   sp.world = pe.world;
   sp.rank = pe.rank;
-  return run_sieve(sv::kCount, sp, P.nseg);
+  return run_sieve(sv::kCount, sp, P.nseg, req);
 }
 
 void peer_detach() {
@@ -474,8 +532,9 @@ int do_stats(uint64_t lo, uint64_t hi, uint64_t *count, uint64_t *sum) {
     if (sum) *sum = P.two ? 2 : 0;
     return 0;
   }
-  TRY(own_base(P.r));
-  TRY(stats_async(P, g.primes.p, g.recips.p, g.nbase.p, g.result.p));
+  BaseReq q;
+  TRY(own_req(P.r, q));
+  TRY(stats_async(P, q.primes, q.recips, q.nbase, g.result.p, &q));
   return fetch_result(count, sum);
 }
 
@@ -486,14 +545,15 @@ int64_t do_bitmap(uint64_t lo, uint64_t hi, uint32_t *out) {
   TRY(ensure_ready());
   const Plan P = make_plan(lo, hi);
   if (P.nbits == 0) return P.two ? 1 : 0;
-  TRY(own_base(P.r));
+  BaseReq q;
+  TRY(own_req(P.r, q));
   const bool dev = is_device_ptr(out);
   uint32_t *dst = out;
   if (!dev) {
     TRY(g.bitmap.ensure(P.words));
     dst = g.bitmap.p;
   }
-  TRY(bitmap_async(P, g.primes.p, g.recips.p, g.nbase.p, dst, g.result.p));
+  TRY(bitmap_async(P, q.primes, q.recips, q.nbase, dst, g.result.p, &q));
   if (!dev)
     CUDA_TRY(cudaMemcpyAsync(out, dst, P.words * 4, cudaMemcpyDeviceToHost, g.stream()));
   uint64_t c = 0;
@@ -518,9 +578,10 @@ int64_t do_primes(uint64_t lo, uint64_t hi, uint64_t *out, uint64_t cap) {
     }
     return P.two ? 1 : 0;
   }
-  TRY(own_base(P.r));
+  BaseReq q;
+  TRY(own_req(P.r, q));
   if (cap == 0) {  // size query: count mode
-    TRY(stats_async(P, g.primes.p, g.recips.p, g.nbase.p, g.result.p));
+    TRY(stats_async(P, q.primes, q.recips, q.nbase, g.result.p, &q));
   } else {
     const bool dev = is_device_ptr(out);
     uint64_t *dst = out;
@@ -544,7 +605,7 @@ int64_t do_primes(uint64_t lo, uint64_t hi, uint64_t *out, uint64_t cap) {
     sp.list_cap = cap;
     sp.lflags = g.lflags.p;
     sp.lepoch = g.lepoch;
-    TRY(run_sieve(sv::kList, sp, P.nseg));
+    TRY(run_sieve(sv::kList, sp, P.nseg, &q));
     uint64_t c = 0;
     TRY(fetch_result(&c, nullptr));
     if (!dev) {
@@ -759,6 +820,21 @@ int sieve_stats_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const ui
   if (!primes || !recips || !nbase || !result) return fail(SIEVE_EINVAL, "NULL buffer");
   TRY(ensure_ready());
   return stats_async(make_plan(lo, hi), primes, recips, nbase, result);
+}
+
+int sieve_stats_base_async(uint64_t lo, uint64_t hi, uint32_t *primes, uint64_t *recips,
+                           uint32_t *nbase, uint64_t cap, int allreduce, uint64_t *result) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  TRY(validate(lo, hi));
+  if (!primes || !recips || !nbase || !result) return fail(SIEVE_EINVAL, "NULL buffer");
+  const Plan P = make_plan(lo, hi);
+  if (cap < base_capacity(P.r)) return fail(SIEVE_EINVAL, "cap %llu < sieve_base_capacity(%llu)",
+                                            (unsigned long long)cap, (unsigned long long)P.r);
+  if (allreduce && g.peer.world == 0) return fail(SIEVE_EINVAL, "no peers attached (sieve_peer_attach)");
+  TRY(ensure_ready());
+  const BaseReq q{primes, recips, nbase, cap, P.r};
+  if (allreduce) return stats_allreduce_async(P, primes, recips, nbase, result, &q);
+  return stats_async(P, primes, recips, nbase, result, &q);
 }
 
 int sieve_bitmap_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const uint64_t *recips,

@@ -9,7 +9,9 @@ one NVSwitch box:
               (reading R10; "average divide data into nodes")
   distribute: rank 0 computes the base primes (K1) and broadcasts ONE packed
               buffer [recips | primes | nbase] (PAPER.md:19's FIFO buffer of
-              data from other nodes becomes a single NCCL broadcast)
+              data from other nodes becomes a single NCCL broadcast); or
+              (broadcast=False) every rank computes its own block's base
+              primes inside its sieve launch (fused A2, no collective)
   sieve     : every rank runs the segmented sieve on its block (CUDA, C ABI)
   gather    : one all-reduce of u64[2] = {count, sum}; two's-complement int64
               addition is bit-identical to u64 addition mod 2^64.  With
@@ -99,6 +101,13 @@ class CudaBackend:
         import paper_1205_4883_b200 as sv
         with _LibraryStreamOrder():
             sv.stats_allreduce_async(a, b, base.primes, base.recips, base.nbase, result)
+
+    def stats_base(self, a, b, base, result, allreduce=False):
+        """A2 (base primes <= isqrt(b-1), into base) and the block's count/sum
+        in one kernel launch; allreduce: the fused peer all-reduce too."""
+        import paper_1205_4883_b200 as sv
+        with _LibraryStreamOrder():
+            sv.stats_base_async(a, b, base.primes, base.recips, base.nbase, result, allreduce)
 
     def peer_handle(self) -> bytes:
         import paper_1205_4883_b200 as sv
@@ -196,19 +205,20 @@ def stats(lo: int, hi: int, group=None, broadcast: bool = True, base: BaseBuffer
         base = alloc_base(be.base_capacity(r), dev)
     if result is None:
         result = torch.zeros(2, dtype=torch.int64, device=dev)
-    if rank == 0 or not broadcast or world == 1:
-        be.base_primes(r, base)
-    if world > 1 and broadcast:
-        dist.broadcast(base.packed, src=0, group=group)
     a, b = block_of(lo, hi, rank, world)
     if fused is None:
         fused = _ATTACHED.get(id(group)) == world
-    if fused:
-        be.stats_allreduce(a, b, base, result)
+    if world > 1 and broadcast:
+        # A9 distribute: rank 0 computes the base primes, one NCCL broadcast
+        if rank == 0:
+            be.base_primes(r, base)
+        dist.broadcast(base.packed, src=0, group=group)
+        (be.stats_allreduce if fused else be.stats)(a, b, base, result)
     else:
-        be.stats(a, b, base, result)
-        if world > 1:
-            dist.all_reduce(result, op=dist.ReduceOp.SUM, group=group)
+        # every rank computes its block's base primes inside its sieve launch
+        be.stats_base(a, b, base, result, fused)
+    if world > 1 and not fused:
+        dist.all_reduce(result, op=dist.ReduceOp.SUM, group=group)
     if not sync:
         return result
     h = result.cpu().tolist()

@@ -59,6 +59,11 @@ class OracleBackend:
         result[0] = D.u64_to_i64(c)
         result[1] = D.u64_to_i64(s)
 
+    def stats_base(self, a, b, base, result, allreduce=False):
+        # the fused launch: this block's own base primes, then its stats
+        self.base_primes(D.isqrt(b - 1) if b >= 2 else 0, base)
+        (self.stats_allreduce if allreduce else self.stats)(a, b, base, result)
+
 
 class OracleGatherBackend:
     """CPU stand-in for CudaGatherBackend (test only)."""
@@ -130,6 +135,7 @@ def _worker(rank, world, port, q, tmpdir=None):
         for lo, hi in [(2, 10**6 + 1), (10**12, 10**12 + 3 * 10**5), (0, 0), (5, 6),
                        (2**63 // 2**16, 2**63 // 2**16 + 10**5)]:
             out[(lo, hi)] = D.stats(lo, hi, backend=be, device=cpu)
+            out[("per-rank base", lo, hi)] = D.stats(lo, hi, broadcast=False, backend=be, device=cpu)
         lo5, hi5 = inputs.config5_intervals(64)
         c, s = D.batch(lo5, hi5, batch_fn=lambda a, b: oracle.batch(a, b, 1), device=cpu)
         out["batch"] = (c.tolist(), s.tolist())
@@ -152,7 +158,8 @@ def _worker(rank, world, port, q, tmpdir=None):
             lo, hi = 10**6 * k + k, 10**6 * k + 6 * 10**4 + 3 * k
             if rng.random() < 0.5:
                 time.sleep(rng.random() * 0.02)
-            out[("F4", lo, hi)] = D.stats(lo, hi, backend=sim, device=cpu)
+            # odd k: the per-rank fused base-prime launch with the fused all-reduce
+            out[("F4", lo, hi)] = D.stats(lo, hi, broadcast=k % 2 == 0, backend=sim, device=cpu)
         out[("F4", 9, 9)] = D.stats(9, 9, backend=sim, device=cpu)
         out["epochs"] = sim.epoch
         D.detach_peers(backend=sim)
@@ -183,7 +190,7 @@ def test_two_rank_gloo_stats_batch_and_wrap():
             assert words == obm.tolist(), key                     # gathered bitmap == whole bitmap
             assert cs == D.bitmap_checksum(obm), key              # all-reduced decomposable checksum
             assert lst == oracle.primes(lo, hi).tolist(), key     # gathered list == whole list
-        elif isinstance(key, tuple) and key[0] == "F4":
+        elif isinstance(key, tuple) and key[0] in ("F4", "per-rank base"):
             assert val == oracle.stats(*key[1:]), key          # one reduction, whole range
         elif isinstance(key, tuple):
             assert val == oracle.stats(*key), key

@@ -57,3 +57,34 @@ def test_base_primes_back_to_back_epochs(dev):
         got, _ = _run(r, dev)
         want = oracle.base_primes(r)
         assert np.array_equal(got, want[want > 2].astype(np.int64)), r
+
+
+@pytest.mark.parametrize("lo,hi", [(2, 10**7 + 1), (0, 10), (2, 3), (10**10 - 10**8, 10**10 + 1),
+                                   (10**12, 10**12 + 10**9), (2**48 - 3 * 10**6, 2**48),
+                                   (3 * 10**13, 3 * 10**13 + 2 * 10**8 + 7)])
+def test_fused_base_launch(dev, lo, hi):
+    """sieve_stats_base_async: A2 inside the sieve launch (or K1 first when a
+    CTA's slice would not fit) -- the base-prime buffers it fills and the
+    stats, against the oracle."""
+    r = D.isqrt(hi - 1) if hi >= 2 else 0
+    base = D.alloc_base(sv.base_capacity(r), dev)
+    base.packed.fill_(-1)
+    res = torch.zeros(2, dtype=torch.int64, device=dev)
+    sv.set_stream(torch.cuda.current_stream())
+    try:
+        for _ in range(2):  # the grid barrier counter must be back at 0 for the second launch
+            sv.stats_base_async(lo, hi, base.primes, base.recips, base.nbase, res)
+            torch.cuda.synchronize()
+            got = [int(x) & ((1 << 64) - 1) for x in res.cpu().tolist()]
+            assert tuple(got) == oracle.stats(lo, hi), (lo, hi)
+    finally:
+        sv.set_stream(None)
+    want = oracle.base_primes(r)
+    want = want[want > 2].astype(np.int64)
+    n = int(base.nbase.item())
+    if hi - lo >= 2:  # an empty odd range launches no sieve: K1 fills the buffers
+        assert n == want.size
+        assert np.array_equal(base.primes[:n].cpu().numpy().astype(np.int64), want)
+        rec = base.recips[:n].cpu().numpy().view(np.uint64)
+        for i in np.random.default_rng(7).choice(n, min(n, 2048), replace=False) if n else []:
+            assert int(rec[i]) == ((1 << 64) - 1) // int(want[i])

@@ -27,7 +27,16 @@ for G in [int(x) for x in os.environ.get("GS", "1,2,4,8").split(",")]:
             torch.cuda.synchronize()
             if i >= 3:
                 bs.append(e[0].elapsed_time(e[1])); ks.append(e[1].elapsed_time(e[2]))
+        fs = []
+        for i in range(13):  # A2 fused into the sieve launch
+            flush.zero_()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            e[0].record(); sv.stats_base_async(a, b, base.primes, base.recips, base.nbase, res); e[1].record()
+            torch.cuda.synchronize()
+            if i >= 3:
+                fs.append(e[0].elapsed_time(e[1]))
         k = statistics.median(ks)
         m = bench.algorithmic_marks(a, b)
         print(f"G={G} rank={g} [{a},{b}) K1={statistics.median(bs)*1e3:.1f}us sieve={k*1e3:.1f}us "
-              f"frac={m / (k / 1e3) / 1e9 / peak:.3f}", flush=True)
+              f"frac={m / (k / 1e3) / 1e9 / peak:.3f} | K1+sieve={(statistics.median(bs) + k)*1e3:.1f}us "
+              f"fused={statistics.median(fs)*1e3:.1f}us", flush=True)
