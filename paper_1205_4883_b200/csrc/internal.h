@@ -127,7 +127,7 @@ struct SieveParams {
   uint64_t out_words;      // words of out
   uint32_t out_vec4;       // out is 16-byte aligned
   uint32_t add_two;        // 2 in [lo, hi): add (1, 2) to the result
-  uint64_t *partials;      // [2 * gridDim.x]
+  uint64_t *partials;      // [2] accumulator of (count, sum): 0 at launch, reset by the last CTA
   unsigned int *done;      // last-block-done ticket (self-resetting)
   uint64_t *result;        // [2] count, sum mod 2^64 (batch: [2 * nintervals])
   const BatchItem *items;  // batch mode

@@ -1139,8 +1139,9 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   }
   if (MODE == kBatch) return;
 
-  // per-CTA partial, then the last CTA to finish reduces all partials in a
-  // fixed order (deterministic) and writes the result.
+  // per-CTA partial added into the launch's accumulator (u64 atomics: exact
+  // mod 2^64, so the order does not matter); the last CTA to finish takes
+  // the total and resets the accumulator for the next launch.
   if (P.prof && threadIdx.x == 0) {
     const unsigned long long t = global_ns();
     atomicMax(P.prof + 107, t);
@@ -1148,21 +1149,22 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   }
   block_sum2(cnt, sum, red);
   if (threadIdx.x == 0) {
-    P.partials[2 * blockIdx.x] = cnt;
-    P.partials[2 * blockIdx.x + 1] = sum;
+    unsigned long long *acc = reinterpret_cast<unsigned long long *>(P.partials);
+    atomicAdd(acc, cnt);
+    atomicAdd(acc + 1, sum);
     __threadfence();
     const unsigned int t = atomicAdd(P.done, 1u);
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (s_last) {
-    __threadfence();
     unsigned long long c = 0, sm = 0;
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-      c += __ldcg(reinterpret_cast<const unsigned long long *>(P.partials) + 2 * b);
-      sm += __ldcg(reinterpret_cast<const unsigned long long *>(P.partials) + 2 * b + 1);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned long long *acc = reinterpret_cast<unsigned long long *>(P.partials);
+      c = atomicExch(acc, 0ull);
+      sm = atomicExch(acc + 1, 0ull);
     }
-    block_sum2(c, sm, red);
     if (threadIdx.x == 0) {
       if (P.add_two) { c += 1; sm += 2; }
       // F4: the cross-GPU all-reduce, fused (peer.cuh); sentinel on timeout

@@ -209,6 +209,8 @@ int ensure_ready() {
   CUDA_TRY(cudaMemcpy(g.tables.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
   TRY(g.done.ensure(1));
   CUDA_TRY(cudaMemset(g.done.p, 0, sizeof(unsigned int)));
+  TRY(g.partials.ensure(2));
+  CUDA_TRY(cudaMemset(g.partials.p, 0, 2 * sizeof(uint64_t)));
   TRY(g.result.ensure(2));
   if (!g.h_res) CUDA_TRY(cudaMallocHost(&g.h_res, 2 * sizeof(uint64_t)));
   g.ready = true;
@@ -419,8 +421,7 @@ int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork, const BaseReq *req =
     sp.recips = req->recips;
     sp.nbase = req->nbase;
   }
-  TRY(g.partials.ensure(2 * (size_t)grid));
-  sp.partials = g.partials.p;
+  sp.partials = g.partials.p;  // [2], zeroed at init, reset by every launch's last CTA
   // not in list mode: its look-back needs the segments of a wave in flight
   // together (round robin), a CTA's contiguous run would serialise it
   if (mode == sv::kCount || mode == sv::kBitmap) TRY(setup_buckets(sp, grid));
