@@ -720,11 +720,20 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
     }
     unsigned long long k = base + incl - cx;
     const uint64_t v0 = a + 64ull * w;
-    while (x) {
-      const uint32_t b = __ffs(x) - 1;
-      x &= x - 1;
-      if (k < P.list_cap) P.list[k] = v0 + 2ull * b;
-      ++k;
+    if (k + cx <= P.list_cap) {  // the whole word fits: no per-prime check
+      uint64_t *dst = P.list + k;
+      while (x) {
+        const uint32_t b = __ffs(x) - 1;
+        x &= x - 1;
+        *dst++ = v0 + 2ull * b;
+      }
+    } else {
+      while (x) {
+        const uint32_t b = __ffs(x) - 1;
+        x &= x - 1;
+        if (k < P.list_cap) P.list[k] = v0 + 2ull * b;
+        ++k;
+      }
     }
     base += __shfl_sync(0xffffffffu, incl, 31);
   }
