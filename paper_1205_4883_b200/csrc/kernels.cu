@@ -207,21 +207,37 @@ struct PrimeRegions {
   uint32_t end;    // first prime > r
 };
 
-// Mark bit `mask` of the words at byte offsets A, A+step, ... < alim of the
-// segment: the hits of one residue class mod 1024 (2 instructions per mark:
-// the address add and the atomic, plus a guard per 4 marks).
-__device__ __forceinline__ void mark_run(uint32_t A, uint32_t alim, uint32_t step, uint32_t mask) {
-  for (; A + 3u * step < alim; A += 4u * step) {
-    red_or(A, mask);
-    red_or(A + step, mask);
-    red_or(A + 2u * step, mask);
-    red_or(A + 3u * step, mask);
+// Multiples of 3 are composite from the wheel (every wheel includes 3), so a
+// prime p's hit n = p m with 3 | m need not be marked: one hit in three.
+// Counting hits k = 0, 1, ... from the segment's first hit n0 = a + 2 j0 =
+// p m0, hit k is p (m0 + 2k), a multiple of 3 iff k = m0 (mod 3), and
+// m0 = n0 p (mod 3) (p^-1 = p mod 3).  a3 = a mod 3.
+__device__ __forceinline__ uint32_t skip_residue(uint32_t a3, uint32_t j0, uint32_t p) {
+  return ((a3 + 2u * j0) * (p % 3u)) % 3u;
+}
+// the two kept offsets {0, 1, 2} \ {skip} of a period of three steps
+__device__ __forceinline__ uint32_t keep_lo(uint32_t skip) { return skip == 0u ? 1u : 0u; }
+__device__ __forceinline__ uint32_t keep_hi(uint32_t skip) { return skip == 2u ? 1u : 2u; }
+
+// Mark bit `mask` of the words at byte offsets A + t step < alim of the
+// segment, t = 0, 1, ... except t = skip (mod 3): the hits of one residue
+// class mod 1024 that are not multiples of 3 (2 instructions per mark: the
+// address add and the atomic, plus a guard per 4 marks).
+__device__ __forceinline__ void mark_run(uint32_t A, uint32_t alim, uint32_t step, uint32_t mask,
+                                         uint32_t skip) {
+  uint32_t A1 = A + keep_lo(skip) * step, A2 = A + keep_hi(skip) * step;  // A1 < A2 < A1 + 3 step
+  const uint32_t s3 = 3u * step;
+  for (; A2 + s3 < alim; A1 += 2u * s3, A2 += 2u * s3) {
+    red_or(A1, mask);
+    red_or(A2, mask);
+    red_or(A1 + s3, mask);
+    red_or(A2 + s3, mask);
   }
-  if (A < alim) {
-    red_or(A, mask);
-    if (A + step < alim) {
-      red_or(A + step, mask);
-      if (A + 2u * step < alim) red_or(A + 2u * step, mask);
+  if (A1 < alim) {
+    red_or(A1, mask);
+    if (A2 < alim) {
+      red_or(A2, mask);
+      if (A1 + s3 < alim) red_or(A1 + s3, mask);
     }
   }
 }
@@ -252,7 +268,9 @@ __device__ __forceinline__ uint32_t class_limit(uint32_t j, uint32_t valid) {
 //  (C)  K < kWarpHits: one prime per lane, unrolled by kLargeILP loads,
 //       except the bucket primes (K < kBucketHits, see bucket_drain) when the
 //       runtime enables buckets.
-// Every atomic of (A1)-(B) is conflict-free; (C) has random banks.  First
+// Every atomic of (A1)-(B) is conflict-free; (C) has random banks.  Hits
+// that are multiples of 3 (k = m0 mod 3, skip_residue) are skipped in every
+// region: one atomic in three.  First
 // hits come from a Barrett reduction, 32 primes per warp at a time, with
 // shuffle broadcast; p^2 >= segment end stops a warp.  Work is dealt
 // statically and evenly: (A2) in pieces round robin, (B) and (C) in
@@ -270,6 +288,7 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t seg_end = a + 2ull * valid;
   const bool whole = (valid & 1023u) == 0;  // every class has the same block limit
+  const uint32_t a3 = (uint32_t)(a % 3u);
 
   // (A1) units (prime, class group), dealt round robin over the warps:
   // unit 32 i + g goes to warp (32 i + g) mod nw, rot = 32 i mod nw
@@ -290,9 +309,11 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
       const uint32_t g0 = warp >= rot ? warp - rot : warp + nw - rot;
       rot += c32;
       if (rot >= nw) rot -= nw;
+      const uint32_t r0 = skip_residue(a3, j0, p);
       for (uint32_t g = g0; g < 32u; g += nw) {
-        const uint32_t j = j0 + (32u * g + lane) * p;  // first hit of class 32 g + lane
-        mark_run(sb + t_addr(j), sb + class_limit(j, valid), 128u * p, t_mask(j));
+        const uint32_t c = 32u * g + lane;  // class c: hits k = c + 1024 t = c + t (mod 3)
+        const uint32_t j = j0 + c * p;      // its first hit
+        mark_run(sb + t_addr(j), sb + class_limit(j, valid), 128u * p, t_mask(j), (r0 + 1026u - c) % 3u);
       }
     }
   }
@@ -313,13 +334,15 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
       uint32_t j = j0 + (lane + 32u * g0) * p;  // first hit of class lane + 32 g0
       uint32_t mask = t_mask(j);
       const uint32_t step = 128u * p, dj = 32u * p;
+      // class c = lane + 32 g skips t = r0 - c (mod 3); c + 32 steps it by +1
+      uint32_t skip = (skip_residue(a3, j0, p) + 1026u - (lane + 32u * g0)) % 3u;
       if (whole) {
         const uint32_t alim = sb + ((j & 31u) << 2) + ((valid >> 10) << 7);
-        for (uint32_t g = g0; g < g1; ++g, j += dj, mask = rotl(mask, p))
-          mark_run(sb + t_addr(j), alim, step, mask);
+        for (uint32_t g = g0; g < g1; ++g, j += dj, mask = rotl(mask, p), skip = skip == 2u ? 0u : skip + 1u)
+          mark_run(sb + t_addr(j), alim, step, mask, skip);
       } else {
-        for (uint32_t g = g0; g < g1; ++g, j += dj, mask = rotl(mask, p))
-          mark_run(sb + t_addr(j), sb + class_limit(j, valid), step, mask);
+        for (uint32_t g = g0; g < g1; ++g, j += dj, mask = rotl(mask, p), skip = skip == 2u ? 0u : skip + 1u)
+          mark_run(sb + t_addr(j), sb + class_limit(j, valid), step, mask, skip);
       }
     }
   }
@@ -355,21 +378,28 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
       // valid a multiple of 32: row < valid / 32 for every bank
       const uint32_t Qlim = w32 ? Qlim32 : sb + (((valid + 31u - (j & 31u)) >> 5) << 2);
       const uint32_t s4 = 4u * p;
-      for (; Q + 3u * s4 < Qlim; Q += 4u * s4) {
-        red_or((Q & ~127u) | b4, mask);
-        mask = rotl(mask, p);
-        red_or(((Q + s4) & ~127u) | b4, mask);
-        mask = rotl(mask, p);
-        red_or(((Q + 2u * s4) & ~127u) | b4, mask);
-        mask = rotl(mask, p);
-        red_or(((Q + 3u * s4) & ~127u) | b4, mask);
-        mask = rotl(mask, p);
+      // lane l's hits k = l + 32 s: multiples of 3 at s = 2 r0 + l (mod 3);
+      // two streams over the kept steps of each period of three
+      const uint32_t sig = (2u * skip_residue(a3, j0, p) + lane) % 3u;
+      const uint32_t o1 = keep_lo(sig), o2 = keep_hi(sig);
+      uint32_t Q1 = Q + o1 * s4, Q2 = Q + o2 * s4;
+      uint32_t m1 = rotl(mask, o1 * p), m2 = rotl(mask, o2 * p);
+      const uint32_t s3 = 3u * s4, p3 = 3u * p;
+      for (; Q2 + s3 < Qlim; Q1 += 2u * s3, Q2 += 2u * s3) {
+        red_or((Q1 & ~127u) | b4, m1);
+        red_or((Q2 & ~127u) | b4, m2);
+        m1 = rotl(m1, p3);
+        m2 = rotl(m2, p3);
+        red_or(((Q1 + s3) & ~127u) | b4, m1);
+        red_or(((Q2 + s3) & ~127u) | b4, m2);
+        m1 = rotl(m1, p3);
+        m2 = rotl(m2, p3);
       }
-      if (Q < Qlim) {  // the last < 4 hits, predicated
-        red_or((Q & ~127u) | b4, mask);
-        if (Q + s4 < Qlim) {
-          red_or(((Q + s4) & ~127u) | b4, rotl(mask, p));
-          if (Q + 2u * s4 < Qlim) red_or(((Q + 2u * s4) & ~127u) | b4, rotl(mask, 2u * p));
+      if (Q1 < Qlim) {  // the last < 4 kept hits, predicated (Q1 < Q2 < Q1 + s3)
+        red_or((Q1 & ~127u) | b4, m1);
+        if (Q2 < Qlim) {
+          red_or((Q2 & ~127u) | b4, m2);
+          if (Q1 + s3 < Qlim) red_or(((Q1 + s3) & ~127u) | b4, rotl(m1, p3));
         }
       }
     }
@@ -405,15 +435,23 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
 #pragma unroll
     for (int u = 0; u < kLargeILP; ++u) {
       if (jk[u] == kNone) break;
-      const uint32_t P4 = 4u * pk[u];
-      uint32_t J = 4u * jk[u] + 32u * sb;
-      for (; J + 3u * P4 < Jlim; J += 4u * P4) {
-        red_or(j_addr(J), j_mask(J));
-        red_or(j_addr(J + P4), j_mask(J + P4));
-        red_or(j_addr(J + 2u * P4), j_mask(J + 2u * P4));
-        red_or(j_addr(J + 3u * P4), j_mask(J + 3u * P4));
+      const uint32_t P4 = 4u * pk[u], S3 = 3u * P4;
+      const uint32_t r0 = skip_residue(a3, jk[u], pk[u]);  // hits k = r0 (mod 3): multiples of 3
+      uint32_t J1 = 4u * jk[u] + 32u * sb + keep_lo(r0) * P4;
+      uint32_t J2 = J1 + (keep_hi(r0) - keep_lo(r0)) * P4;  // J1 < J2 < J1 + S3
+      for (; J2 + S3 < Jlim; J1 += 2u * S3, J2 += 2u * S3) {
+        red_or(j_addr(J1), j_mask(J1));
+        red_or(j_addr(J2), j_mask(J2));
+        red_or(j_addr(J1 + S3), j_mask(J1 + S3));
+        red_or(j_addr(J2 + S3), j_mask(J2 + S3));
       }
-      for (; J < Jlim; J += P4) red_or(j_addr(J), j_mask(J));
+      if (J1 < Jlim) {
+        red_or(j_addr(J1), j_mask(J1));
+        if (J2 < Jlim) {
+          red_or(j_addr(J2), j_mask(J2));
+          if (J1 + S3 < Jlim) red_or(j_addr(J1 + S3), j_mask(J1 + S3));
+        }
+      }
     }
   }
   if (prof) {  // per-warp busy cycles of the regions (diagnostics only)
