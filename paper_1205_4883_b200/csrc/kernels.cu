@@ -353,6 +353,15 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // (4 row) & ~127 | 4 bank and the mask rotates by p.
   const bool w32 = (valid & 31u) == 0;
   const uint32_t Qlim32 = sb + ((valid >> 5) << 2);
+  // lane l skips s = 2 r0 + l (mod 3): for each r0, the lane's first kept
+  // step o1 and the gap d to its second (2 bits per r0, indexed by 2 r0)
+  uint32_t o1t = 0, dt = 0;
+#pragma unroll
+  for (uint32_t r = 0; r < 3u; ++r) {
+    const uint32_t sig = (2u * r + lane) % 3u;
+    o1t |= keep_lo(sig) << (2u * r);
+    dt |= (keep_hi(sig) - keep_lo(sig)) << (2u * r);
+  }
   // prime nw m + (m even ? w : nw - 1 - w) to warp w (boustrophedon: the
   // primes grow with the index, so a plain i mod nw loads the low warps)
   for (uint32_t ib = R.cls; ib < b_end; ib += 32u * nw) {
@@ -361,29 +370,30 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
     if (i < b_end) {
       pl = __ldg(primes + i);
       jl = first_hit(a, seg_end, pl, __ldg(recips + i));
+      if (jl != kNone) jl |= skip_residue(a3, jl, pl) << 30;  // j0 < 2^22: r0 rides in bits 30-31
     }
     bool stop = false;
     for (uint32_t k = 0; k < 32u; ++k) {
       const uint32_t p = __shfl_sync(0xffffffffu, pl, k);
-      const uint32_t j0 = __shfl_sync(0xffffffffu, jl, k);
-      if (j0 == kNone) { stop = true; break; }  // and so for every later prime
-      const uint32_t j = j0 + lane * p;
+      const uint32_t jp = __shfl_sync(0xffffffffu, jl, k);
+      if (jp == kNone) { stop = true; break; }  // and so for every later prime
+      // lane l's hits k = l + 32 s: multiples of 3 at s = 2 r0 + l (mod 3);
+      // two streams over the kept steps (o1, o1 + d) of each period of three
+      const uint32_t r2 = (jp >> 29) & 6u;  // 2 r0
+      const uint32_t o1 = (o1t >> r2) & 3u, d = (dt >> r2) & 3u;
+      const uint32_t j = (jp & 0x3FFFFFFFu) + (lane + 32u * o1) * p;  // the lane's first kept hit
       const uint32_t row = j >> 5;
       const uint32_t b4 = (j << 2) & 124u;  // 4 bank
       // Q = shared byte address of the hit's block plus 4 (row & 31): the
       // 128-byte aligned base keeps (Q & ~127) | b4 the hit's word
-      uint32_t Q = sb + 4u * row;
-      uint32_t mask = __funnelshift_l(0u, 1u, row);
+      uint32_t Q1 = sb + 4u * row;
+      uint32_t m1 = __funnelshift_l(0u, 1u, row);
       // slot < valid <=> row < ceil((valid - bank) / 32) (0 when bank >= valid);
       // valid a multiple of 32: row < valid / 32 for every bank
       const uint32_t Qlim = w32 ? Qlim32 : sb + (((valid + 31u - (j & 31u)) >> 5) << 2);
       const uint32_t s4 = 4u * p;
-      // lane l's hits k = l + 32 s: multiples of 3 at s = 2 r0 + l (mod 3);
-      // two streams over the kept steps of each period of three
-      const uint32_t sig = (2u * skip_residue(a3, j0, p) + lane) % 3u;
-      const uint32_t o1 = keep_lo(sig), o2 = keep_hi(sig);
-      uint32_t Q1 = Q + o1 * s4, Q2 = Q + o2 * s4;
-      uint32_t m1 = rotl(mask, o1 * p), m2 = rotl(mask, o2 * p);
+      uint32_t Q2 = Q1 + d * s4;
+      uint32_t m2 = rotl(m1, d * p);
       const uint32_t s3 = 3u * s4, p3 = 3u * p;
       for (; Q2 + s3 < Qlim; Q1 += 2u * s3, Q2 += 2u * s3) {
         red_or((Q1 & ~127u) | b4, m1);
