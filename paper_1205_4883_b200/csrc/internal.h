@@ -59,11 +59,11 @@ constexpr uint64_t kOddPrimesBelow64 =
 //   kWarpHits <= K < kClassHits: warp per prime, lanes on consecutive hits
 //   K < kWarpHits             : lane per prime
 #ifndef SIEVE_UNIT_HITS
-#define SIEVE_UNIT_HITS 32768
+#define SIEVE_UNIT_HITS 49152  // A/B-tuned with the 3-skip (32768 -> 49152)
 #endif
 constexpr uint32_t kUnitHits = SIEVE_UNIT_HITS;
 #ifndef SIEVE_CLASS_HITS
-#define SIEVE_CLASS_HITS 16384
+#define SIEVE_CLASS_HITS 24576  // A/B-tuned with the 3-skip (16384 -> 24576)
 #endif
 constexpr uint32_t kClassHits = SIEVE_CLASS_HITS;
 #ifndef SIEVE_A2_PARTS
