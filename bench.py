@@ -47,7 +47,7 @@ SMEM_LANES_PER_CLK = 32              # one conflict-free shared-memory wavefront
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--seg-kb", type=int, default=0)
@@ -115,6 +115,19 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+
+    def sample_now(self):
+        """One sample from the calling thread (the timed loop calls it after
+        enqueuing its steps, while the GPU still runs them)."""
+        if self.ok:
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
 
     def summary(self):
         if not self.ok or not self.samples:
@@ -314,6 +327,9 @@ def main():
             with torch.cuda.stream(stream):
                 flush.zero_()  # L2 flush, outside the events
             step(ev[k])
+            if k == args.steps // 2:
+                sampler.sample_now()  # the GPU is busy with the steps enqueued so far
+        sampler.sample_now()
         torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall0
     if world > 1:
