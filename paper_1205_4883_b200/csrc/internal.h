@@ -76,6 +76,12 @@ constexpr uint32_t kA2Parts = SIEVE_A2_PARTS;  // pieces per (A2) prime (divides
 constexpr uint32_t kWarpHits = SIEVE_WARP_HITS;
 // step A5: primes with fewer than kBucketHits hits per full segment (p > S /
 // kBucketHits) go through per-segment buckets when enabled (option buckets)
+// (C) primes with >= kC15Hits hits left in the segment also skip the
+// multiples of 5 (8 kept hits per 15); fewer hits: only the multiples of 3
+#ifndef SIEVE_C15_HITS
+#define SIEVE_C15_HITS 32  // A/B: 16, 32, 48 -> 32
+#endif
+constexpr uint32_t kC15Hits = SIEVE_C15_HITS;
 #ifndef SIEVE_BUCKET_HITS
 #define SIEVE_BUCKET_HITS 1
 #endif

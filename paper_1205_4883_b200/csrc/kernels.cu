@@ -215,6 +215,23 @@ struct PrimeRegions {
 __device__ __forceinline__ uint32_t skip_residue(uint32_t a3, uint32_t j0, uint32_t p) {
   return ((a3 + 2u * j0) * (p % 3u)) % 3u;
 }
+// 5 is in every wheel too: hit k is a multiple of 5 iff k = 2 m0 (mod 5),
+// m0 = n0 p^-1 (mod 5); a5 = a mod 5, p^-1 mod 5 from the nibble table
+// 1 -> 1, 2 -> 3, 3 -> 2, 4 -> 4.
+__device__ __forceinline__ uint32_t skip_residue5(uint32_t a5, uint32_t j0, uint32_t p) {
+  const uint32_t inv = (0x42310u >> (4u * (p % 5u))) & 7u;
+  return ((a5 + 2u * j0) * 2u * inv) % 5u;
+}
+// the 8 kept hit offsets of a period of 15 (k mod 15 not = r3 mod 3 and not
+// = r5 mod 5), ascending, as nibbles of one word: table entry 5 r3 + r5
+__device__ __forceinline__ uint32_t kept15(uint32_t r3, uint32_t r5) {
+  uint32_t keep = ~((0x1249u << r3) | (0x421u << r5)) & 0x7FFFu, w = 0;
+  for (int i = 0; i < 8; ++i) {
+    w |= (uint32_t)(__ffs(keep) - 1) << (4 * i);
+    keep &= keep - 1u;
+  }
+  return w;
+}
 // the two kept offsets {0, 1, 2} \ {skip} of a period of three steps
 __device__ __forceinline__ uint32_t keep_lo(uint32_t skip) { return skip == 0u ? 1u : 0u; }
 __device__ __forceinline__ uint32_t keep_hi(uint32_t skip) { return skip == 2u ? 1u : 2u; }
@@ -278,7 +295,8 @@ __device__ __forceinline__ uint32_t class_limit(uint32_t j, uint32_t valid) {
 __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__restrict__ primes,
                                              const uint64_t *__restrict__ recips,
                                              const PrimeRegions R, uint32_t flags,
-                                             uint64_t a, uint32_t valid, unsigned long long *prof) {
+                                             uint64_t a, uint32_t valid, unsigned long long *prof,
+                                             const uint32_t *k15) {
   // diagnostics (sieve_debug_set_flags): drop whole regions (wrong results)
   const uint32_t a1_end = flags & kFlagSkipA ? R.start : R.unit;
   const uint32_t a2_end = flags & kFlagSkipA ? R.unit : R.cls;
@@ -288,7 +306,7 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint64_t seg_end = a + 2ull * valid;
   const bool whole = (valid & 1023u) == 0;  // every class has the same block limit
-  const uint32_t a3 = (uint32_t)(a % 3u);
+  const uint32_t a3 = (uint32_t)(a % 3u), a5 = (uint32_t)(a % 5u);
 
   // (A1) units (prime, class group), dealt round robin over the warps:
   // unit 32 i + g goes to warp (32 i + g) mod nw, rot = 32 i mod nw
@@ -447,6 +465,22 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
       if (jk[u] == kNone) break;
       const uint32_t P4 = 4u * pk[u], S3 = 3u * P4;
       const uint32_t r0 = skip_residue(a3, jk[u], pk[u]);  // hits k = r0 (mod 3): multiples of 3
+      if ((uint64_t)(Jlim - 4u * jk[u] - 32u * sb) >= (uint64_t)kC15Hits * P4) {
+        // many hits left: skip the multiples of 5 too, 8 kept per period of 15
+        const uint32_t nib = k15[5u * r0 + skip_residue5(a5, jk[u], pk[u])];
+        uint32_t off[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) off[q] = ((nib >> (4 * q)) & 15u) * P4;
+        uint32_t J = 4u * jk[u] + 32u * sb;
+        for (; J + off[7] < Jlim; J += 5u * S3) {  // whole periods
+#pragma unroll
+          for (int q = 0; q < 8; ++q) red_or(j_addr(J + off[q]), j_mask(J + off[q]));
+        }
+#pragma unroll
+        for (int q = 0; q < 7; ++q)  // the last partial period (offsets ascending)
+          if (J + off[q] < Jlim) red_or(j_addr(J + off[q]), j_mask(J + off[q]));
+        continue;
+      }
       uint32_t J1 = 4u * jk[u] + 32u * sb + keep_lo(r0) * P4;
       uint32_t J2 = J1 + (keep_hi(r0) - keep_lo(r0)) * P4;  // J1 < J2 < J1 + S3
       for (; J2 + S3 < Jlim; J1 += 2u * S3, J2 += 2u * S3) {
@@ -1111,6 +1145,8 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     atomicMax(P.prof + 104, ~t);
     atomicMax(P.prof + 105, t);
   }
+  __shared__ uint32_t s_k15[15];  // kept15(r3, r5) at 5 r3 + r5
+  if (threadIdx.x < 15u) s_k15[threadIdx.x] = kept15(threadIdx.x / 5u, threadIdx.x % 5u);
   for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
   if (MODE != kBatch && P.bprimes) base_phase(P, seg);  // fused A2 (scratch below tab)
   compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
@@ -1157,7 +1193,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     wheel_init<NG>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
-    if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof);
+    if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);
     if (buckets) {
       bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s), valid);
       bq = bq + 1u == P.ring ? 0u : bq + 1u;
