@@ -59,7 +59,7 @@ typedef struct sieve_options {
     uint32_t segment_kb;  /* maximum shared-memory segment size in KiB, in [4, 224] (default 208);
                              a call cuts [lo, hi) into equal segments of at most this size, a whole
                              number of waves of the persistent grid (at least 8 KiB) */
-    uint32_t wheel;       /* wheel bound w (pre-sieved primes 3..w): 11, 17, 23, 31, 41 or 47 (default 41);
+    uint32_t wheel;       /* wheel bound w (pre-sieved primes 3..w): 11, 17, 23, 31, 41 or 47 (default 31);
                              segment + wheel tables must fit 226 KiB of shared memory */
     uint32_t ctas_per_sm; /* resident CTAs per SM for the sieve kernel (default: occupancy maximum) */
     uint32_t threads;     /* threads per CTA: a multiple of 64 in [256, 1024] (default 1024) */

@@ -52,7 +52,7 @@ def test_validation_before_device():
         sv.set_options(segment_kb=208, wheel=47)  # 208 KiB + 25 KiB of tables > 226 KiB
     assert sv.get_options()["segment_kb"] == 64
     sv.set_options()
-    assert sv.get_options() == {"segment_kb": 208, "wheel": 41, "ctas_per_sm": 0, "threads": 1024,
+    assert sv.get_options() == {"segment_kb": 208, "wheel": 31, "ctas_per_sm": 0, "threads": 1024,
                                  "buckets": 0}
 
 
