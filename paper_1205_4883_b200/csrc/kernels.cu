@@ -990,11 +990,19 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
 // Grid-wide barrier of a cooperative launch: thread 0 of each CTA arrives
 // on *bar and waits for `target` arrivals (the counter only grows within a
 // launch: the n-th barrier waits for n * gridDim.x).
-__device__ __forceinline__ void grid_barrier(unsigned int *bar, unsigned int target) {
+// Split-phase grid barrier of a cooperative launch: arrive (thread 0 of
+// each CTA counts in on *bar after the CTA's writes), do independent work,
+// then wait for `target` arrivals (the counter only grows within a launch:
+// the n-th barrier waits for n * gridDim.x).
+__device__ __forceinline__ void grid_arrive(unsigned int *bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(bar, 1u);
+  }
+}
+__device__ __forceinline__ void grid_wait(unsigned int *bar, unsigned int target) {
+  if (threadIdx.x == 0) {
     unsigned int v;
     for (;;) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
@@ -1012,7 +1020,10 @@ __device__ __forceinline__ void grid_barrier(unsigned int *bar, unsigned int tar
 // below the wheel tables, used here as scratch), counts its
 // primes and publishes the count; after a grid barrier it places them by the
 // counts of the slices before it and writes primes and reciprocals; a second
-// grid barrier makes the whole list visible before any CTA reads it.
+// grid barrier makes the whole list visible before any CTA reads it.  Both
+// barriers are split (arrive ... wait): the staging and reciprocals run
+// while the other CTAs arrive at the first, and the caller initialises its
+// first segment (wheel) between arrive and wait of the second.
 __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) {
   __shared__ uint32_t s_w[32];
   __shared__ unsigned long long s_base;  // this slice's first list index
@@ -1055,26 +1066,10 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
     P.bcounts[blockIdx.x] = t;
     if (P.prof) atomicMax(P.prof + 110, global_ns());
   }
-  grid_barrier(P.gbar, G);
-  if (P.prof && tid == 0) atomicMax(P.prof + 111, global_ns());
-  if (warp == 0) {  // this slice's offset and the total
-    unsigned long long before = 0, all = 0;
-    for (uint32_t k = lane; k < G; k += 32u) {
-      const unsigned long long v = __ldcg(P.bcounts + k);
-      all += v;
-      if (k < blockIdx.x) before += v;
-    }
-    before = warp_sum_u64(before);
-    all = warp_sum_u64(all);
-    if (lane == 0) {
-      s_base = before;
-      if (blockIdx.x == 0) *P.bnbase = (uint32_t)min(all, (unsigned long long)P.bcap);
-    }
-  }
-  __syncthreads();
-  // ordered emission: the slice's primes staged in shared memory by a block
-  // scan per row of blockDim.x words, then one prime (and its reciprocal)
-  // per thread, coalesced
+  grid_arrive(P.gbar);
+  // while the other CTAs arrive: the slice's primes staged in order (a block
+  // scan per row of blockDim.x words) and the first two per thread with
+  // their reciprocals in registers
   uint32_t *stage = bm + nwd;  // <= nbits / 3 + 2 entries (host-checked space)
   uint32_t o = 0;
   for (uint32_t w0 = 0; w0 < nwd; w0 += blockDim.x) {
@@ -1104,8 +1099,36 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
     o += row;
   }
   __syncthreads();
+  const uint32_t t1 = tid + blockDim.x;
+  const uint32_t p0 = tid < o ? stage[tid] : 3u, p1 = t1 < o ? stage[t1] : 3u;
+  const uint64_t q0 = recip_of(p0), q1 = recip_of(p1);
+  grid_wait(P.gbar, G);
+  if (P.prof && tid == 0) atomicMax(P.prof + 111, global_ns());
+  if (warp == 0) {  // this slice's offset and the total
+    unsigned long long before = 0, all = 0;
+    for (uint32_t k = lane; k < G; k += 32u) {
+      const unsigned long long v = __ldcg(P.bcounts + k);
+      all += v;
+      if (k < blockIdx.x) before += v;
+    }
+    before = warp_sum_u64(before);
+    all = warp_sum_u64(all);
+    if (lane == 0) {
+      s_base = before;
+      if (blockIdx.x == 0) *P.bnbase = (uint32_t)min(all, (unsigned long long)P.bcap);
+    }
+  }
+  __syncthreads();
   const unsigned long long base = s_base;
-  for (uint32_t t = tid; t < o; t += blockDim.x) {
+  if (tid < o && base + tid < P.bcap) {
+    P.bprimes[base + tid] = p0;
+    P.brecips[base + tid] = q0;
+  }
+  if (t1 < o && base + t1 < P.bcap) {
+    P.bprimes[base + t1] = p1;
+    P.brecips[base + t1] = q1;
+  }
+  for (uint32_t t = t1 + blockDim.x; t < o; t += blockDim.x) {  // large r only
     if (base + t < P.bcap) {
       const uint32_t p = stage[t];
       P.bprimes[base + t] = p;
@@ -1113,8 +1136,7 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
     }
   }
   if (P.prof && tid == 0) atomicMax(P.prof + 117, global_ns());
-  grid_barrier(P.gbar, 2u * G);
-  if (P.prof && tid == 0) atomicMax(P.prof + 118, global_ns());
+  grid_arrive(P.gbar);  // the caller does independent work, then grid_wait(2 G)
 }
 
 // ---------------------------------------------------------------------------
@@ -1148,12 +1170,6 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   __shared__ uint32_t s_k15[15];  // kept15(r3, r5) at 5 r3 + r5
   if (threadIdx.x < 15u) s_k15[threadIdx.x] = kept15(threadIdx.x / 5u, threadIdx.x % 5u);
   for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
-  if (MODE != kBatch && P.bprimes) base_phase(P, seg);  // fused A2 (scratch below tab)
-  compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
-  __syncthreads();
-  if (P.prof && threadIdx.x == 0) atomicMax(P.prof + 106, global_ns());
-
-  unsigned long long cnt = 0, sum = 0;
   // segments round robin; with the buckets of step A5 a range is sieved in
   // contiguous runs (the buckets carry each large prime from one segment of
   // the run to the next)
@@ -1161,6 +1177,24 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   const uint64_t s_begin = buckets ? blockIdx.x * P.nseg / gridDim.x : blockIdx.x;
   const uint64_t s_end = buckets ? (blockIdx.x + 1ull) * P.nseg / gridDim.x : P.nseg;
   const uint64_t s_step = buckets ? 1u : gridDim.x;
+  // fused A2: the base primes, then the first segment's wheel pattern while
+  // the other CTAs finish theirs (between arrive and wait of the last barrier)
+  const bool pre_init = MODE != kBatch && P.bprimes && s_begin < s_end;
+  if (MODE != kBatch && P.bprimes) {
+    base_phase(P, seg);
+    if (pre_init) {
+      const uint64_t bit0 = s_begin * (uint64_t)P.seg_bits, left = P.nbits - bit0;
+      wheel_init<NG>(seg, tab, P.o0, bit0, left < P.seg_bits ? (uint32_t)left : P.seg_bits,
+                     P.o0 + 2ull * bit0);
+    }
+    grid_wait(P.gbar, 2u * gridDim.x);
+    if (P.prof && threadIdx.x == 0) atomicMax(P.prof + 118, global_ns());
+  }
+  compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
+  __syncthreads();
+  if (P.prof && threadIdx.x == 0) atomicMax(P.prof + 106, global_ns());
+
+  unsigned long long cnt = 0, sum = 0;
   uint32_t bcnt = 0;  // lane t: fill count of the warp's bucket slot t
   uint32_t bq = 0;    // ring slot of the current segment
   if (buckets && s_begin < s_end) {
@@ -1190,7 +1224,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       a = o0 + 2ull * bit0;
     }
     const long long c0 = P.prof ? clock64() : 0;
-    wheel_init<NG>(seg, tab, o0, bit0, valid, a);
+    if (!(pre_init && s == s_begin)) wheel_init<NG>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
     if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);
