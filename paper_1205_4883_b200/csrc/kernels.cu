@@ -1117,6 +1117,33 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
       s_base = before;
       if (blockIdx.x == 0) *P.bnbase = (uint32_t)min(all, (unsigned long long)P.bcap);
     }
+    // the region boundaries of compute_regions (first index with a prime
+    // > x = number of odd primes <= x), published by the slice holding x;
+    // P.bcounts[G + k], k = 1 unit, 2 class, 3 warp, 4 bucket
+    unsigned int *reg = P.bcounts + G;
+#pragma unroll
+    for (uint32_t k = 1; k < 5u; ++k) {
+      const uint64_t x = k == 1u ? P.seg_bits / kUnitHits
+                       : k == 2u ? P.seg_bits / kClassHits
+                       : k == 3u ? P.seg_bits / kWarpHits
+                       : P.buckets ? P.seg_bits / kBucketHits : ~0ull;
+      const uint64_t ix = x >= 3u ? (x - 1u) / 2u : 0u;  // largest i with 2i + 1 <= x
+      if (ix == 0 || ix > imax) {  // below 3, or past r: 0 or every prime
+        if (blockIdx.x == 0 && lane == 0) reg[k] = ix == 0 ? 0u : (uint32_t)all;
+        continue;
+      }
+      if (ix < i0 || ix >= (uint64_t)i0 + nbits) continue;  // another slice's
+      const uint32_t last = (uint32_t)(ix - i0);               // bits 0 .. last count
+      uint32_t cnt = 0;
+      for (uint32_t w = lane; w <= last / 32u; w += 32u) {
+        uint32_t xw = word(w);
+        if (w == last / 32u && (last & 31u) != 31u) xw &= (2u << (last & 31u)) - 1u;
+        cnt += __popc(xw);
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o2);
+      if (lane == 0) reg[k] = (uint32_t)before + cnt;
+    }
   }
   __syncthreads();
   const unsigned long long base = s_base;
@@ -1190,7 +1217,19 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     grid_wait(P.gbar, 2u * gridDim.x);
     if (P.prof && threadIdx.x == 0) atomicMax(P.prof + 118, global_ns());
   }
-  compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
+  if (MODE != kBatch && P.bprimes) {  // fused A2 published the boundaries
+    if (threadIdx.x == 0) {
+      const unsigned int *reg = P.bcounts + gridDim.x;
+      sR.end = __ldcg(P.bnbase);
+      sR.start = min(wheel_nprimes(NG), sR.end);
+      sR.unit = max(sR.start, min(sR.end, __ldcg(reg + 1)));
+      sR.cls = max(sR.unit, min(sR.end, __ldcg(reg + 2)));
+      sR.warp = max(sR.cls, min(sR.end, __ldcg(reg + 3)));
+      sR.big = max(sR.warp, min(sR.end, __ldcg(reg + 4)));
+    }
+  } else {
+    compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
+  }
   __syncthreads();
   if (P.prof && threadIdx.x == 0) atomicMax(P.prof + 106, global_ns());
 
