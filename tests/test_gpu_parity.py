@@ -311,3 +311,21 @@ def test_top_of_range_2_48(seg_kb, buckets):
     bm, cb = sv.bitmap(lo, hi)
     obm, oc, _ = oracle.bitmap(lo, hi)
     assert cb == oc and np.array_equal(bm, obm)
+
+
+@pytest.mark.parametrize("seg_kb,wheel", [(4, 11), (24, 31), (208, 31), (40, 47), (104, 17)])
+def test_skip_residues_random_offsets(seg_kb, wheel):
+    """The marking loops skip the hits that are multiples of 3 (and of 5 in
+    long (C) walks): which hits those are depends on lo mod 3, lo mod 5, the
+    segment offsets and p mod 3 / mod 5.  Random lo of every residue mod 30,
+    odd segment sizes and several wheels, count + sum + bitmap vs the oracle."""
+    sv.set_options(segment_kb=seg_kb, wheel=wheel)
+    rng = np.random.default_rng(1000 + seg_kb + wheel)
+    for k in range(12):
+        lo = int(rng.integers(10**6, 2**40)) // 30 * 30 + (7 * k + seg_kb) % 30
+        hi = lo + int(rng.integers(1, 3 * 10**6))
+        assert sv.stats(lo, hi) == oracle.stats(lo, hi), (lo, hi)
+        if k % 4 == 0:
+            bm, c = sv.bitmap(lo, hi)
+            obm, _, _ = oracle.bitmap(lo, hi)
+            assert np.array_equal(bm[: obm.size], obm), (lo, hi)
