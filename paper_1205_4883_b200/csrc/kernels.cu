@@ -22,6 +22,7 @@
 // write-back inverts it so that the bitmap has 1 = prime (reading R5), and
 // transposes each 1024-slot block back to the natural bit order.
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -203,6 +204,7 @@ struct PrimeRegions {
   uint32_t unit;   // first prime with fewer than kUnitHits hits per full segment
   uint32_t cls;    // first prime with fewer than kClassHits hits per full segment
   uint32_t warp;   // first prime with fewer than kWarpHits hits per full segment
+  uint32_t few;    // first prime with fewer than kC15Hits hits per full segment
   uint32_t big;    // first bucket prime (fewer than kBucketHits hits; = end without buckets)
   uint32_t end;    // first prime > r
 };
@@ -442,62 +444,69 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // of slot j is (J >> 5) & ~127 | J & 127 and its bit is (J >> 7) & 31 (the
   // base term is a multiple of 4096, invisible to both).
   const uint32_t Jlim = 4u * valid + 32u * sb;
-  // round m of nt primes: thread t takes prime m nt + (m even ? t : nt - 1 - t)
-  for (uint32_t k0 = R.warp; k0 < c_end; k0 += kLargeILP * blockDim.x) {
-    uint32_t pk[kLargeILP], jk[kLargeILP];
-    uint64_t rk[kLargeILP];
+  // round m of nt primes: thread t takes prime m nt + (m even ? t : nt - 1 - t).
+  // Primes [R.warp, few) have >= kC15Hits hits per full segment and skip the
+  // multiples of 5 as well (8 kept hits per period of 15); [few, c_end) skip
+  // the multiples of 3 only.  Two loops: no per-lane branch on the walk kind.
+  const uint32_t few = min(R.few, c_end);
+  auto c_loop = [&](uint32_t cb, uint32_t ce, auto by15) {
+    for (uint32_t k0 = cb; k0 < ce; k0 += kLargeILP * blockDim.x) {
+      uint32_t pk[kLargeILP], jk[kLargeILP];
+      uint64_t rk[kLargeILP];
 #pragma unroll
-    for (int u = 0; u < kLargeILP; ++u) {
-      const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
-      const uint32_t k = min(ku, c_end - 1u);
-      pk[u] = __ldg(primes + k);
-      rk[u] = __ldg(recips + k);
-    }
+      for (int u = 0; u < kLargeILP; ++u) {
+        const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+        const uint32_t k = min(ku, ce - 1u);
+        pk[u] = __ldg(primes + k);
+        rk[u] = __ldg(recips + k);
+      }
 #pragma unroll
-    for (int u = 0; u < kLargeILP; ++u) {
-      jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
-      const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
-      if (ku >= c_end) jk[u] = kNone;
-    }
-    if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
+      for (int u = 0; u < kLargeILP; ++u) {
+        jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
+        const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+        if (ku >= ce) jk[u] = kNone;
+      }
+      if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
 #pragma unroll
-    for (int u = 0; u < kLargeILP; ++u) {
-      if (jk[u] == kNone) break;
-      const uint32_t P4 = 4u * pk[u], S3 = 3u * P4;
-      const uint32_t r0 = skip_residue(a3, jk[u], pk[u]);  // hits k = r0 (mod 3): multiples of 3
-      if ((uint64_t)(Jlim - 4u * jk[u] - 32u * sb) >= (uint64_t)kC15Hits * P4) {
-        // many hits left: skip the multiples of 5 too, 8 kept per period of 15
-        const uint32_t nib = k15[5u * r0 + skip_residue5(a5, jk[u], pk[u])];
-        uint32_t off[8];
+      for (int u = 0; u < kLargeILP; ++u) {
+        if (jk[u] == kNone) break;
+        const uint32_t P4 = 4u * pk[u], S3 = 3u * P4;
+        const uint32_t r0 = skip_residue(a3, jk[u], pk[u]);  // hits k = r0 (mod 3): multiples of 3
+        if constexpr (decltype(by15)::value) {
+          const uint32_t nib = k15[5u * r0 + skip_residue5(a5, jk[u], pk[u])];
+          uint32_t off[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) off[q] = ((nib >> (4 * q)) & 15u) * P4;
-        uint32_t J = 4u * jk[u] + 32u * sb;
-        for (; J + off[7] < Jlim; J += 5u * S3) {  // whole periods
+          for (int q = 0; q < 8; ++q) off[q] = ((nib >> (4 * q)) & 15u) * P4;
+          uint32_t J = 4u * jk[u] + 32u * sb;
+          for (; J + off[7] < Jlim; J += 5u * S3) {  // whole periods
 #pragma unroll
-          for (int q = 0; q < 8; ++q) red_or(j_addr(J + off[q]), j_mask(J + off[q]));
+            for (int q = 0; q < 8; ++q) red_or(j_addr(J + off[q]), j_mask(J + off[q]));
+          }
+#pragma unroll
+          for (int q = 0; q < 7; ++q)  // the last partial period (offsets ascending)
+            if (J + off[q] < Jlim) red_or(j_addr(J + off[q]), j_mask(J + off[q]));
+        } else {
+          uint32_t J1 = 4u * jk[u] + 32u * sb + keep_lo(r0) * P4;
+          uint32_t J2 = J1 + (keep_hi(r0) - keep_lo(r0)) * P4;  // J1 < J2 < J1 + S3
+          for (; J2 + S3 < Jlim; J1 += 2u * S3, J2 += 2u * S3) {
+            red_or(j_addr(J1), j_mask(J1));
+            red_or(j_addr(J2), j_mask(J2));
+            red_or(j_addr(J1 + S3), j_mask(J1 + S3));
+            red_or(j_addr(J2 + S3), j_mask(J2 + S3));
+          }
+          if (J1 < Jlim) {
+            red_or(j_addr(J1), j_mask(J1));
+            if (J2 < Jlim) {
+              red_or(j_addr(J2), j_mask(J2));
+              if (J1 + S3 < Jlim) red_or(j_addr(J1 + S3), j_mask(J1 + S3));
+            }
+          }
         }
-#pragma unroll
-        for (int q = 0; q < 7; ++q)  // the last partial period (offsets ascending)
-          if (J + off[q] < Jlim) red_or(j_addr(J + off[q]), j_mask(J + off[q]));
-        continue;
-      }
-      uint32_t J1 = 4u * jk[u] + 32u * sb + keep_lo(r0) * P4;
-      uint32_t J2 = J1 + (keep_hi(r0) - keep_lo(r0)) * P4;  // J1 < J2 < J1 + S3
-      for (; J2 + S3 < Jlim; J1 += 2u * S3, J2 += 2u * S3) {
-        red_or(j_addr(J1), j_mask(J1));
-        red_or(j_addr(J2), j_mask(J2));
-        red_or(j_addr(J1 + S3), j_mask(J1 + S3));
-        red_or(j_addr(J2 + S3), j_mask(J2 + S3));
-      }
-      if (J1 < Jlim) {
-        red_or(j_addr(J1), j_mask(J1));
-        if (J2 < Jlim) {
-          red_or(j_addr(J2), j_mask(J2));
-          if (J1 + S3 < Jlim) red_or(j_addr(J1 + S3), j_mask(J1 + S3));
-        }
       }
     }
-  }
+  };
+  c_loop(R.warp, few, std::true_type{});
+  c_loop(few, c_end, std::false_type{});
   if (prof) {  // per-warp busy cycles of the regions (diagnostics only)
     const long long t4 = clock64();
     if ((threadIdx.x & 31u) == 0) {
@@ -967,12 +976,13 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
                                                 bool only_end) {
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t nb = *P.nbase;
-  if (warp < (only_end ? 1u : 5u)) {
+  if (warp < (only_end ? 1u : 6u)) {
     const uint64_t x = warp == 0 ? (uint64_t)r
                      : warp == 1 ? P.seg_bits / kUnitHits
                      : warp == 2 ? P.seg_bits / kClassHits
                      : warp == 3 ? P.seg_bits / kWarpHits
-                     : P.buckets ? P.seg_bits / kBucketHits : ~0ull;
+                     : warp == 4 ? (P.buckets ? P.seg_bits / kBucketHits : ~0ull)
+                     : P.seg_bits / kC15Hits;
     const uint32_t u = warp_upper_bound(P.primes, nb, x);
     if ((threadIdx.x & 31u) == 0) scratch[warp] = u;
   }
@@ -984,6 +994,7 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
     R.cls = max(R.unit, min(R.end, scratch[2]));
     R.warp = max(R.cls, min(R.end, scratch[3]));
     R.big = max(R.warp, min(R.end, scratch[4]));
+    R.few = max(R.warp, min(R.big, scratch[5]));
   }
 }
 
@@ -1119,14 +1130,15 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
     }
     // the region boundaries of compute_regions (first index with a prime
     // > x = number of odd primes <= x), published by the slice holding x;
-    // P.bcounts[G + k], k = 1 unit, 2 class, 3 warp, 4 bucket
+    // P.bcounts[G + k], k = 1 unit, 2 class, 3 warp, 4 bucket, 5 few
     unsigned int *reg = P.bcounts + G;
 #pragma unroll
-    for (uint32_t k = 1; k < 5u; ++k) {
+    for (uint32_t k = 1; k < 6u; ++k) {
       const uint64_t x = k == 1u ? P.seg_bits / kUnitHits
                        : k == 2u ? P.seg_bits / kClassHits
                        : k == 3u ? P.seg_bits / kWarpHits
-                       : P.buckets ? P.seg_bits / kBucketHits : ~0ull;
+                       : k == 4u ? (P.buckets ? P.seg_bits / kBucketHits : ~0ull)
+                       : P.seg_bits / kC15Hits;
       const uint64_t ix = x >= 3u ? (x - 1u) / 2u : 0u;  // largest i with 2i + 1 <= x
       if (ix == 0 || ix > imax) {  // below 3, or past r: 0 or every prime
         if (blockIdx.x == 0 && lane == 0) reg[k] = ix == 0 ? 0u : (uint32_t)all;
@@ -1184,7 +1196,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   __shared__ unsigned long long red[64];
   __shared__ PrimeRegions sR;
   __shared__ uint32_t s_last;
-  __shared__ uint32_t s_ub[5];
+  __shared__ uint32_t s_ub[6];
   __shared__ uint32_t s_wc[33];            // list mode: warp counts / offsets, segment total
   __shared__ unsigned long long s_off;     // list mode: the segment's place in the list
 
@@ -1226,6 +1238,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       sR.cls = max(sR.unit, min(sR.end, __ldcg(reg + 2)));
       sR.warp = max(sR.cls, min(sR.end, __ldcg(reg + 3)));
       sR.big = max(sR.warp, min(sR.end, __ldcg(reg + 4)));
+      sR.few = max(sR.warp, min(sR.big, __ldcg(reg + 5)));
     }
   } else {
     compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
@@ -1254,6 +1267,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       Ri.unit = min(Ri.unit, Ri.end);
       Ri.cls = min(Ri.cls, Ri.end);
       Ri.warp = min(Ri.warp, Ri.end);
+      Ri.few = min(Ri.few, Ri.end);
       Ri.big = min(Ri.big, Ri.end);
     } else {
       o0 = P.o0;

@@ -19,7 +19,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "paper_1205_4883_b200", "csrc", "kernels.cu")
 LIB = os.path.join(ROOT, "paper_1205_4883_b200", "libsieve.so")
 rep = sys.argv[1]
-fn = sys.argv[2] if len(sys.argv) > 2 else "_ZN2sv7k_sieveILi5ELi0EEEvNS_11SieveParamsE"
+
+def _captured_kernel(report):
+    """Mangled name of the k_sieve<NG, MODE> instantiation in the report."""
+    out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    name = rows[2][rows[0].index("Kernel Name")]
+    m = re.search(r"k_sieve<(\d+), (\d+)>", name)
+    if not m:
+        raise SystemExit(f"not a k_sieve capture: {name}")
+    return f"_ZN2sv7k_sieveILi{m.group(1)}ELi{m.group(2)}EEEvNS_11SieveParamsE"
+
+
+fn = sys.argv[2] if len(sys.argv) > 2 else _captured_kernel(rep)
 
 # ---- region line ranges from markers in the source
 src = open(SRC).read().split("\n")
