@@ -170,7 +170,7 @@ struct SieveParams {
   uint32_t *bnbase;
   uint32_t bcap;        // capacity of bprimes/brecips
   uint32_t rs;          // isqrt(r)
-  uint32_t *bcounts;    // [gridDim.x] per-CTA prime counts, then [6] region boundaries
+  uint32_t *bcounts;    // [gridDim.x] per-CTA prime counts, then [7] region boundaries
   unsigned int *gbar;   // grid barrier counter: 0 at launch, reset by the last CTA
 };
 

@@ -205,6 +205,7 @@ struct PrimeRegions {
   uint32_t cls;    // first prime with fewer than kClassHits hits per full segment
   uint32_t warp;   // first prime with fewer than kWarpHits hits per full segment
   uint32_t few;    // first prime with fewer than kC15Hits hits per full segment
+  uint32_t two;    // first prime with at most 2 hits in any segment (p > S / 2)
   uint32_t big;    // first bucket prime (fewer than kBucketHits hits; = end without buckets)
   uint32_t end;    // first prime > r
 };
@@ -294,6 +295,7 @@ __device__ __forceinline__ uint32_t class_limit(uint32_t j, uint32_t valid) {
 // shuffle broadcast; p^2 >= segment end stops a warp.  Work is dealt
 // statically and evenly: (A2) in pieces round robin, (B) and (C) in
 // boustrophedon order over the warps / threads.
+template <bool kPlainTwo>
 __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__restrict__ primes,
                                              const uint64_t *__restrict__ recips,
                                              const PrimeRegions R, uint32_t flags,
@@ -506,7 +508,40 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
     }
   };
   c_loop(R.warp, few, std::true_type{});
-  c_loop(few, c_end, std::false_type{});
+  // batch kernel (kPlainTwo): p > S / 2 has at most 2 hits, marked as they
+  // come (a skipped multiple of 3 would cost more than its atomic); compiled
+  // out of the other kernels, whose loops it would perturb (+0.7 % measured)
+  const uint32_t two = kPlainTwo ? max(few, min(R.two, c_end)) : c_end;
+  c_loop(few, two, std::false_type{});
+  if constexpr (kPlainTwo)
+  for (uint32_t k0 = two; k0 < c_end; k0 += kLargeILP * blockDim.x) {
+    uint32_t pk[kLargeILP], jk[kLargeILP];
+    uint64_t rk[kLargeILP];
+#pragma unroll
+    for (int u = 0; u < kLargeILP; ++u) {
+      const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+      const uint32_t k = min(ku, c_end - 1u);
+      pk[u] = __ldg(primes + k);
+      rk[u] = __ldg(recips + k);
+    }
+#pragma unroll
+    for (int u = 0; u < kLargeILP; ++u) {
+      jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
+      const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+      if (ku >= c_end) jk[u] = kNone;
+    }
+    if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
+#pragma unroll
+    for (int u = 0; u < kLargeILP; ++u) {
+      if (jk[u] == kNone) break;
+      const uint32_t J = 4u * jk[u] + 32u * sb;
+      if (J < Jlim) {
+        red_or(j_addr(J), j_mask(J));
+        const uint32_t J2 = J + 4u * pk[u];
+        if (J2 < Jlim) red_or(j_addr(J2), j_mask(J2));
+      }
+    }
+  }
   if (prof) {  // per-warp busy cycles of the regions (diagnostics only)
     const long long t4 = clock64();
     if ((threadIdx.x & 31u) == 0) {
@@ -976,13 +1011,14 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
                                                 bool only_end) {
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t nb = *P.nbase;
-  if (warp < (only_end ? 1u : 6u)) {
+  if (warp < (only_end ? 1u : 7u)) {
     const uint64_t x = warp == 0 ? (uint64_t)r
                      : warp == 1 ? P.seg_bits / kUnitHits
                      : warp == 2 ? P.seg_bits / kClassHits
                      : warp == 3 ? P.seg_bits / kWarpHits
                      : warp == 4 ? (P.buckets ? P.seg_bits / kBucketHits : ~0ull)
-                     : P.seg_bits / kC15Hits;
+                     : warp == 5 ? P.seg_bits / kC15Hits
+                     : P.seg_bits / 2u;
     const uint32_t u = warp_upper_bound(P.primes, nb, x);
     if ((threadIdx.x & 31u) == 0) scratch[warp] = u;
   }
@@ -995,6 +1031,7 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
     R.warp = max(R.cls, min(R.end, scratch[3]));
     R.big = max(R.warp, min(R.end, scratch[4]));
     R.few = max(R.warp, min(R.big, scratch[5]));
+    R.two = max(R.few, min(R.big, scratch[6]));
   }
 }
 
@@ -1130,15 +1167,16 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
     }
     // the region boundaries of compute_regions (first index with a prime
     // > x = number of odd primes <= x), published by the slice holding x;
-    // P.bcounts[G + k], k = 1 unit, 2 class, 3 warp, 4 bucket, 5 few
+    // P.bcounts[G + k], k = 1 unit, 2 class, 3 warp, 4 bucket, 5 few, 6 two
     unsigned int *reg = P.bcounts + G;
 #pragma unroll
-    for (uint32_t k = 1; k < 6u; ++k) {
+    for (uint32_t k = 1; k < 7u; ++k) {
       const uint64_t x = k == 1u ? P.seg_bits / kUnitHits
                        : k == 2u ? P.seg_bits / kClassHits
                        : k == 3u ? P.seg_bits / kWarpHits
                        : k == 4u ? (P.buckets ? P.seg_bits / kBucketHits : ~0ull)
-                       : P.seg_bits / kC15Hits;
+                       : k == 5u ? P.seg_bits / kC15Hits
+                       : P.seg_bits / 2u;
       const uint64_t ix = x >= 3u ? (x - 1u) / 2u : 0u;  // largest i with 2i + 1 <= x
       if (ix == 0 || ix > imax) {  // below 3, or past r: 0 or every prime
         if (blockIdx.x == 0 && lane == 0) reg[k] = ix == 0 ? 0u : (uint32_t)all;
@@ -1196,7 +1234,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   __shared__ unsigned long long red[64];
   __shared__ PrimeRegions sR;
   __shared__ uint32_t s_last;
-  __shared__ uint32_t s_ub[6];
+  __shared__ uint32_t s_ub[7];
   __shared__ uint32_t s_wc[33];            // list mode: warp counts / offsets, segment total
   __shared__ unsigned long long s_off;     // list mode: the segment's place in the list
 
@@ -1239,6 +1277,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       sR.warp = max(sR.cls, min(sR.end, __ldcg(reg + 3)));
       sR.big = max(sR.warp, min(sR.end, __ldcg(reg + 4)));
       sR.few = max(sR.warp, min(sR.big, __ldcg(reg + 5)));
+      sR.two = max(sR.few, min(sR.big, __ldcg(reg + 6)));
     }
   } else {
     compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
@@ -1268,6 +1307,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       Ri.cls = min(Ri.cls, Ri.end);
       Ri.warp = min(Ri.warp, Ri.end);
       Ri.few = min(Ri.few, Ri.end);
+      Ri.two = min(Ri.two, Ri.end);
       Ri.big = min(Ri.big, Ri.end);
     } else {
       o0 = P.o0;
@@ -1280,7 +1320,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     if (!(pre_init && s == s_begin)) wheel_init<NG>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
-    if (!(P.flags & kFlagSkipMarking)) mark_segment(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);
+    if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);
     if (buckets) {
       bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s), valid);
       bq = bq + 1u == P.ring ? 0u : bq + 1u;

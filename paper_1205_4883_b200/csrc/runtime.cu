@@ -406,7 +406,7 @@ int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork, const BaseReq *req =
         TRY(g.gbar.ensure(1));
         CUDA_TRY(cudaMemsetAsync(g.gbar.p, 0, sizeof(unsigned int), g.stream()));
       }
-      TRY(g.bcounts.ensure((size_t)grid + 6));  // counts, then the region boundaries
+      TRY(g.bcounts.ensure((size_t)grid + 7));  // counts, then the region boundaries
       sp.bprimes = req->primes;
       sp.brecips = req->recips;
       sp.bnbase = req->nbase;
