@@ -82,6 +82,12 @@ constexpr uint32_t kWarpHits = SIEVE_WARP_HITS;
 #define SIEVE_C15_HITS 32  // A/B: 16, 32, 48 -> 32
 #endif
 constexpr uint32_t kC15Hits = SIEVE_C15_HITS;
+// batch kernel: (C) primes with at most kPlainHits hits per segment are
+// marked without the multiple-of-3 skip
+#ifndef SIEVE_PLAIN_HITS
+#define SIEVE_PLAIN_HITS 8  // A/B on config 5: 2 -> 6.49, 4 -> 6.40, 8 -> 6.34, 16 -> 6.37, 32 -> 6.40 ms
+#endif
+constexpr uint32_t kPlainHits = SIEVE_PLAIN_HITS;
 #ifndef SIEVE_BUCKET_HITS
 #define SIEVE_BUCKET_HITS 1
 #endif

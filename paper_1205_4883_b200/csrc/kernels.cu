@@ -508,8 +508,9 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
     }
   };
   c_loop(R.warp, few, std::true_type{});
-  // batch kernel (kPlainTwo): p > S / 2 has at most 2 hits, marked as they
-  // come (a skipped multiple of 3 would cost more than its atomic); compiled
+  // batch kernel (kPlainTwo): p > S / kPlainHits has at most kPlainHits hits,
+  // marked as they come (skipping a multiple of 3 would cost more than its
+  // atomic); compiled
   // out of the other kernels, whose loops it would perturb (+0.7 % measured)
   const uint32_t two = kPlainTwo ? max(few, min(R.two, c_end)) : c_end;
   c_loop(few, two, std::false_type{});
@@ -534,12 +535,8 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
 #pragma unroll
     for (int u = 0; u < kLargeILP; ++u) {
       if (jk[u] == kNone) break;
-      const uint32_t J = 4u * jk[u] + 32u * sb;
-      if (J < Jlim) {
-        red_or(j_addr(J), j_mask(J));
-        const uint32_t J2 = J + 4u * pk[u];
-        if (J2 < Jlim) red_or(j_addr(J2), j_mask(J2));
-      }
+      const uint32_t P4 = 4u * pk[u];
+      for (uint32_t J = 4u * jk[u] + 32u * sb; J < Jlim; J += P4) red_or(j_addr(J), j_mask(J));
     }
   }
   if (prof) {  // per-warp busy cycles of the regions (diagnostics only)
@@ -1018,7 +1015,7 @@ __device__ __forceinline__ void compute_regions(const SieveParams &P, uint32_t r
                      : warp == 3 ? P.seg_bits / kWarpHits
                      : warp == 4 ? (P.buckets ? P.seg_bits / kBucketHits : ~0ull)
                      : warp == 5 ? P.seg_bits / kC15Hits
-                     : P.seg_bits / 2u;
+                     : P.seg_bits / kPlainHits;
     const uint32_t u = warp_upper_bound(P.primes, nb, x);
     if ((threadIdx.x & 31u) == 0) scratch[warp] = u;
   }
@@ -1176,7 +1173,7 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
                        : k == 3u ? P.seg_bits / kWarpHits
                        : k == 4u ? (P.buckets ? P.seg_bits / kBucketHits : ~0ull)
                        : k == 5u ? P.seg_bits / kC15Hits
-                       : P.seg_bits / 2u;
+                       : P.seg_bits / kPlainHits;
       const uint64_t ix = x >= 3u ? (x - 1u) / 2u : 0u;  // largest i with 2i + 1 <= x
       if (ix == 0 || ix > imax) {  // below 3, or past r: 0 or every prime
         if (blockIdx.x == 0 && lane == 0) reg[k] = ix == 0 ? 0u : (uint32_t)all;
