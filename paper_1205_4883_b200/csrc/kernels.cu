@@ -801,33 +801,51 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if (lane == 0) s_wc[warp] = c;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t t = 0;
-    for (uint32_t k = 0; k < nw; ++k) {
-      const uint32_t x = s_wc[k];
-      s_wc[k] = t;  // exclusive warp offsets
-      t += x;
-    }
-    s_wc[32] = t;
+  if (warp == 0) {
+    // segment total and exclusive warp offsets (lane 0), then the decoupled
+    // look-back by the whole warp: 32 predecessor flags per step, the
+    // nearest inclusive one found by a ballot, the aggregates before it
+    // summed by a warp reduction (a one-thread walk would read up to a wave
+    // of flags one L2 round trip at a time)
     volatile unsigned long long *fl = P.lflags;
     const unsigned long long tag = (unsigned long long)P.lepoch << 48;
-    unsigned long long pre = 0;  // the list offset of this segment's first prime
-    if (s == 0) {
-      pre = P.add_two ? 1ull : 0ull;  // list[0] = 2
-      fl[0] = tag | ((pre + t) << 2) | kFlagIncl;
-    } else {
-      fl[s] = tag | ((unsigned long long)t << 2) | kFlagAgg;
-      for (uint64_t j = s; j-- > 0;) {
-        unsigned long long f;
-        do { f = fl[j]; } while ((f >> 48) != P.lepoch);  // not yet published in this launch
-        pre += (f >> 2) & ((1ull << 46) - 1);
-        if ((f & 3u) == kFlagIncl) break;
+    uint32_t t = 0;
+    if (lane == 0) {
+      for (uint32_t k = 0; k < nw; ++k) {
+        const uint32_t x = s_wc[k];
+        s_wc[k] = t;  // exclusive warp offsets
+        t += x;
       }
-      __threadfence();
-      fl[s] = tag | ((pre + t) << 2) | kFlagIncl;
+      s_wc[32] = t;
+      if (s == 0) {
+        const unsigned long long pre0 = P.add_two ? 1ull : 0ull;  // list[0] = 2
+        fl[0] = tag | ((pre0 + t) << 2) | kFlagIncl;
+        *s_off = pre0;
+        if (P.add_two && P.list_cap > 0) P.list[0] = 2;
+      } else {
+        fl[s] = tag | ((unsigned long long)t << 2) | kFlagAgg;
+      }
     }
-    *s_off = pre;
-    if (s == 0 && P.add_two && P.list_cap > 0) P.list[0] = 2;
+    if (s > 0) {
+      unsigned long long pre = 0;
+      for (int64_t j = (int64_t)s - 1;; j -= 32) {
+        const int64_t idx = j - (int64_t)lane;  // lane 0 the nearest
+        unsigned long long f = 0;
+        if (idx >= 0) {
+          do { f = fl[idx]; } while ((f >> 48) != P.lepoch);  // not yet published in this launch
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, idx >= 0 && (f & 3u) == kFlagIncl);
+        const uint32_t stop = incl ? (uint32_t)(__ffs(incl) - 1) : 31u;
+        unsigned long long v = (idx >= 0 && lane <= stop) ? ((f >> 2) & ((1ull << 46) - 1)) : 0ull;
+        pre += warp_sum_u64(v);
+        if (incl) break;  // segment 0 is always inclusive: the walk ends
+      }
+      if (lane == 0) {
+        __threadfence();
+        fl[s] = tag | ((pre + s_wc[32]) << 2) | kFlagIncl;
+        *s_off = pre;
+      }
+    }
   }
   __syncthreads();
   unsigned long long base = *s_off + s_wc[warp];
