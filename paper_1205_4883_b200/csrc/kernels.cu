@@ -285,16 +285,19 @@ __device__ __forceinline__ uint32_t class_limit(uint32_t j, uint32_t valid) {
 //       a rotation of the mask and an add: slot + 32 p).
 //  (B)  kWarpHits <= K < kClassHits: one prime per warp; lane l takes the
 //       hits l + 32 s (row += p, mask rotated by p per hit).
-//  (C)  K < kWarpHits: one prime per lane, unrolled by kLargeILP loads,
-//       except the bucket primes (K < kBucketHits, see bucket_drain) when the
-//       runtime enables buckets.
+//  (C)  K < kWarpHits: one prime per lane, unrolled by kLargeILP loads, in
+//       up to three loops over index ranges: K >= kC15Hits [R.warp, R.few)
+//       skips the multiples of 3 and 5 (8 kept hits per 15), then the
+//       multiples of 3 only, and in the batch kernel K <= kPlainHits
+//       [R.two, ...) plainly; the bucket primes (K < kBucketHits, see
+//       bucket_drain) when the runtime enables buckets.
 // Every atomic of (A1)-(B) is conflict-free; (C) has random banks.  Hits
 // that are multiples of 3 (k = m0 mod 3, skip_residue) are skipped in every
-// region: one atomic in three.  First
-// hits come from a Barrett reduction, 32 primes per warp at a time, with
-// shuffle broadcast; p^2 >= segment end stops a warp.  Work is dealt
-// statically and evenly: (A2) in pieces round robin, (B) and (C) in
-// boustrophedon order over the warps / threads.
+// region: one atomic in three (the wheel marked them).  First hits come
+// from a Barrett reduction, 32 primes per warp at a time, with shuffle
+// broadcast; p^2 >= segment end stops a warp.  Work is dealt statically and
+// evenly: (A2) in pieces round robin, (B) and (C) in boustrophedon order over
+// the warps / threads.
 template <bool kPlainTwo>
 __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__restrict__ primes,
                                              const uint64_t *__restrict__ recips,
