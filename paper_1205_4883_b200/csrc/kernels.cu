@@ -741,7 +741,11 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
   uint32_t k = 0;
   for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x, ++k) {
     const uint4 v = seg4[q];
-    const uint32_t x0 = ~v.x, x1 = ~v.y, x2 = ~v.z, x3 = ~v.w;
+    // count mode counts the composite (set) bits and converts at the end
+    // (every statistic below is linear in the per-position counts); bitmap
+    // mode needs the prime words themselves for the stores
+    const uint32_t x0 = kNatural ? ~v.x : v.x, x1 = kNatural ? ~v.y : v.y;
+    const uint32_t x2 = kNatural ? ~v.z : v.z, x3 = kNatural ? ~v.w : v.w;
     const uint32_t c0 = __popc(x0), c1 = __popc(x1), c2 = __popc(x2), c3 = __popc(x3);
     const uint32_t cq = c0 + c1 + c2 + c3;
     C += cq;
@@ -771,9 +775,15 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
     }
   }
   // sum of bit positions over all set bits = sum_k 2^k bit_index_sum(plane_k)
-  const uint32_t Bs = bit_index_sum(ones) + 2u * bit_index_sum(twos) + 4u * bit_index_sum(fours) +
-                      8u * bit_index_sum(p8) + 16u * bit_index_sum(p16) + 32u * bit_index_sum(p32) +
-                      64u * bit_index_sum(p64) + 128u * bit_index_sum(p128);
+  uint32_t Bs = bit_index_sum(ones) + 2u * bit_index_sum(twos) + 4u * bit_index_sum(fours) +
+                8u * bit_index_sum(p8) + 16u * bit_index_sum(p16) + 32u * bit_index_sum(p32) +
+                64u * bit_index_sum(p64) + 128u * bit_index_sum(p128);
+  if (!kNatural) {  // composite -> prime over the thread's k quads (128 bits each)
+    C = 128u * k - C;                  // set bits
+    Q = 64u * k * (k - 1u) - Q;        // sum of (quad index) x (set bits), 128 sum_{i<k} i
+    X = 192u * k - X;                  // sum of e c_e: 32 (1 + 2 + 3) per quad
+    Bs = 4u * 496u * k - Bs;           // per bit position: 4 k bits, positions sum to 496
+  }
   // sum of 128 q over set bits, q = tid + k nt
   const uint64_t Jq = 128ull * ((uint64_t)threadIdx.x * C + (uint64_t)blockDim.x * Q);
   const uint64_t J = kNatural ? Jq + 32ull * X + Bs
