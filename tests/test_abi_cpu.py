@@ -6,7 +6,6 @@ import re
 import pytest
 
 import paper_1205_4883_b200 as sv
-from paper_1205_4883_b200 import _abi
 
 HEADER = __import__("os").path.join(__import__("os").path.dirname(__file__), "..", "include", "sieve.h")
 

@@ -6,7 +6,6 @@ into this rank's slab before the launch, and checks the slot this rank
 published into the "peer" slab after it.  The protocol across real processes
 is exercised on CPU in test_dist_gloo.py (same slot/epoch/parity logic on
 shared memory)."""
-import numpy as np
 import pytest
 import torch
 

@@ -6,7 +6,6 @@ Carmichael numbers below 2000 (561, 1105, 1729: SPEC.md carmichael_scan)."""
 import math
 
 import numpy as np
-import pytest
 
 import inputs
 import oracle

@@ -1,10 +1,8 @@
 """Quick timings for regression checks: config 4 count at 32 KiB segments and
 config 5 batch (host API), with library/options from the environment
 (SIEVE_LIBRARY, WHEEL)."""
-import os, statistics, sys, time
+import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
-import torch
 import inputs
 import paper_1205_4883_b200 as sv
 w = int(os.environ.get("WHEEL", "0"))
