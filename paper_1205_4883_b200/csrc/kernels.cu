@@ -1274,7 +1274,15 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   }
   __shared__ uint32_t s_k15[15];  // kept15(r3, r5) at 5 r3 + r5
   if (threadIdx.x < 15u) s_k15[threadIdx.x] = kept15(threadIdx.x / 5u, threadIdx.x % 5u);
-  for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
+  // wheel tables to shared memory; with the fused A2, warps >= 2 copy them
+  // while warps 0-1 run its mini-sieve of the small primes (small_primes
+  // syncs the block before anything reads them)
+  if (MODE != kBatch && P.bprimes) {
+    if (threadIdx.x >= 64u)
+      for (uint32_t i = threadIdx.x - 64u; i < tables_words(NG); i += blockDim.x - 64u) tab[i] = P.tables[i];
+  } else {
+    for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
+  }
   // segments round robin; with the buckets of step A5 a range is sieved in
   // contiguous runs (the buckets carry each large prime from one segment of
   // the run to the next)
