@@ -875,11 +875,24 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
     unsigned long long k = base + incl - cx;
     const uint64_t v0 = a + 64ull * w;
     if (k + cx <= P.list_cap) {  // the whole word fits: no per-prime check
+      // two primes per 16-byte store once the address is 16-byte aligned:
+      // the emission is bound by the number of store instructions
       uint64_t *dst = P.list + k;
-      while (x) {
-        const uint32_t b = __ffs(x) - 1;
+      if ((reinterpret_cast<uintptr_t>(dst) & 8u) && x) {
+        *dst++ = v0 + 2ull * (uint32_t)(__ffs(x) - 1);
         x &= x - 1;
-        *dst++ = v0 + 2ull * b;
+      }
+      while (x) {
+        const uint32_t b1 = __ffs(x) - 1;
+        x &= x - 1;
+        if (x) {
+          const uint32_t b2 = __ffs(x) - 1;
+          x &= x - 1;
+          *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(v0 + 2ull * b1, v0 + 2ull * b2);
+          dst += 2;
+        } else {
+          *dst++ = v0 + 2ull * b1;
+        }
       }
     } else {
       while (x) {

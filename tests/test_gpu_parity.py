@@ -138,6 +138,12 @@ def test_primes_list_truncation_and_device_out():
     _, c1 = sv.primes(lo, hi, out=d)
     assert c1 == full.size
     assert np.array_equal(d.cpu().numpy().view(np.uint64), full)
+    # an output 8 bytes past a 16-byte boundary (the emission pairs primes
+    # into 16-byte stores once aligned)
+    d2 = torch.zeros(full.size + 1, dtype=torch.int64, device="cuda")
+    _, c2 = sv.primes(lo, hi, cap=full.size, out=d2[1:])
+    assert c2 == full.size
+    assert np.array_equal(d2[1:].cpu().numpy().view(np.uint64), full) and int(d2[0]) == 0
     w = sv.bitmap_words(lo, hi)
     db = torch.zeros(w, dtype=torch.int32, device="cuda")
     _, cb = sv.bitmap(lo, hi, out=db)

@@ -30,22 +30,23 @@ with tempfile.TemporaryDirectory() as d:
     cub = [f for f in os.listdir(d) if f.startswith("kernels") and f.endswith(".cubin")]
     dis = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(d, sorted(cub)[-1])],
                          capture_output=True, text=True).stdout
-inside, line, off2l = False, None, {}
+inside, chain, line, off2l = False, [], None, {}
 for L in dis.split("\n"):
     if L.startswith("//----") and ".text." in L:
         inside = kname in L
         continue
     if not inside:
         continue
-    m = re.findall(r'"([^"]+)", line (\d+)', L)
-    if L.strip().startswith("//## File") and m:
-        ks = [int(x) for f, x in m if f.endswith("kernels.cu")]
-        if ks:
-            line = ks[0]
+    if L.strip().startswith("//## File"):
+        # the lines before an instruction, innermost first
+        chain += [int(x) for f, x in re.findall(r'"([^"]+)", line (\d+)', L) if f.endswith("kernels.cu")]
         continue
     m2 = re.match(r"\s+/\*([0-9a-f]{4,})\*/", L)
     if m2:
+        if chain:
+            line = chain[0]
         off2l[int(m2.group(1), 16)] = line
+        chain = []
 
 agg = defaultdict(lambda: [0.0, 0.0])
 for r in data:
