@@ -67,7 +67,7 @@ constexpr uint32_t kUnitHits = SIEVE_UNIT_HITS;
 #endif
 constexpr uint32_t kClassHits = SIEVE_CLASS_HITS;
 #ifndef SIEVE_A2_PARTS
-#define SIEVE_A2_PARTS 8
+#define SIEVE_A2_PARTS 4  // A/B after the skips and w = 31: 1, 2, 4, 8, 16 -> 4 (config 3 -1.8 %)
 #endif
 constexpr uint32_t kA2Parts = SIEVE_A2_PARTS;  // pieces per (A2) prime (divides 32)
 #ifndef SIEVE_WARP_HITS
