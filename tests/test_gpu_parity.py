@@ -335,3 +335,28 @@ def test_skip_residues_random_offsets(seg_kb, wheel):
             bm, c = sv.bitmap(lo, hi)
             obm, _, _ = oracle.bitmap(lo, hi)
             assert np.array_equal(bm[: obm.size], obm), (lo, hi)
+
+
+def test_batch_edge_intervals():
+    """Batch with duplicates, overlaps, empty and one-element intervals,
+    intervals containing 2 / the wheel primes / 1, and a 2^48 top one."""
+    iv = [(0, 0), (5, 5), (2, 3), (0, 2), (1, 60), (30, 50), (30, 50), (10**6, 10**6 + 1),
+          (10**6 - 17, 10**6 + 10**5), (10**6, 10**6 + 10**5), (2**48 - 10**5, 2**48),
+          (10**12 - 1, 10**12 + 1), (3, 4), (41, 48), (10**9 + 7, 10**9 + 8)]
+    lo = np.array([a for a, _ in iv], dtype=np.uint64)
+    hi = np.array([b for _, b in iv], dtype=np.uint64)
+    c, s = sv.batch(lo, hi)
+    for k, (a, b) in enumerate(iv):
+        assert (int(c[k]), int(s[k])) == oracle.stats(a, b), (a, b)
+
+
+@pytest.mark.parametrize("lo,hi", [(2, 48), (40, 43), (1, 3), (29, 32), (2, 10**6), (999_983, 10**6 + 7)])
+def test_small_ranges_fused_sync_paths(lo, hi):
+    """Ranges around the wheel primes and tiny ranges through the synchronous
+    APIs (fused base-prime launch) in all three modes."""
+    assert sv.stats(lo, hi) == oracle.stats(lo, hi)
+    bm, c = sv.bitmap(lo, hi)
+    obm, oc, _ = oracle.bitmap(lo, hi)
+    assert c == oc and np.array_equal(bm[: obm.size], obm)
+    lst, n = sv.primes(lo, hi)
+    assert np.array_equal(lst[:n], oracle.primes(lo, hi))
