@@ -115,3 +115,30 @@ def test_attach_validation(dev):
     with pytest.raises(sv.SieveError):  # nothing attached
         res = torch.zeros(2, dtype=torch.int64, device=dev)
         sv.stats_allreduce_async(10, 100, own, own, own, res)
+
+
+@pytest.mark.parametrize("rank", [0, 1])
+@pytest.mark.parametrize("lo,hi", [(2, 10**9 + 1), (10**12, 10**12 + 6 * 10**6 + 1), (2, 30)])
+def test_world2_simulated_peer_fused_base(dev, rank, lo, hi):
+    """The N > 1 production step: base primes, sieve and all-reduce in one
+    cooperative launch (sieve_stats_base_async with allreduce), the peer's
+    slot written by the test as in test_world2_simulated_peer."""
+    _same_stream()
+    own = torch.zeros(sv.PEER_SLAB_BYTES // 8, dtype=torch.int64, device=dev)
+    other = torch.zeros_like(own)
+    slabs = [own, other] if rank == 0 else [other, own]
+    sv.peer_attach_ptrs(slabs, rank, timeout_ms=5000)
+    a, b = D.block_of(lo, hi, rank, 2)
+    pa, pb = D.block_of(lo, hi, 1 - rank, 2)
+    r = D.isqrt(hi - 1) if hi >= 2 else 0
+    base = D.alloc_base(sv.base_capacity(r), dev)
+    res = torch.zeros(2, dtype=torch.int64, device=dev)
+    want = oracle.stats(lo, hi)
+    pc, ps = oracle.stats(pa, pb)
+    for it in range(2):
+        e = sv.peer_epoch() + 1
+        slot = SLOT * ((e & 1) * sv.MAX_PEERS + (1 - rank))
+        own[slot: slot + 3] = torch.tensor([_i64(pc), _i64(ps), e], dtype=torch.int64)
+        sv.stats_base_async(a, b, base.primes, base.recips, base.nbase, res, allreduce=True)
+        torch.cuda.synchronize()
+        assert (_u64(res[0]), _u64(res[1])) == want, (it, a, b)
