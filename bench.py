@@ -269,12 +269,11 @@ def main():
         return bool(t.item())
 
     if fused:
-        try:
-            D.attach_peers(timeout_ms=2000)
-            ok = True
-        except Exception as ex:  # e.g. CUDA IPC unavailable in this container
-            print(f"rank {rank}: fused all-reduce unavailable ({ex})", file=sys.stderr)
-            ok = False
+        # every rank completes the attach collectives even if its own attach
+        # fails (e.g. CUDA IPC unavailable); the ranks then agree
+        ok = D.attach_peers(timeout_ms=2000)
+        if not ok:
+            print(f"rank {rank}: fused all-reduce unavailable", file=sys.stderr)
         if not all_ok(ok):
             fused = False
             D.detach_peers()

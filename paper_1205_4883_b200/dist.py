@@ -132,22 +132,36 @@ def attach_peers(group=None, timeout_ms: int = 10000, backend=None) -> bool:
     IPC handle, the handles are all-gathered over the host in rank order and
     every rank opens its peers' slabs; a barrier makes every slab zeroed
     before anyone's first fused launch.  Later stats(..., fused=True) calls
-    on this group all-reduce inside the sieve kernel."""
+    on this group all-reduce inside the sieve kernel.  Every rank takes part
+    in every collective even when its own export or attach fails, so a local
+    failure cannot leave the others waiting; returns whether THIS rank is
+    attached (callers agree across ranks before using it)."""
     import torch.distributed as dist
     be = backend if backend is not None else CudaBackend()
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    mine = be.peer_handle()
+    ok = True
+    try:
+        mine = be.peer_handle()
+    except Exception:  # noqa: BLE001 -- reported through the return value
+        mine, ok = b"", False
     if world > 1:
         handles = [None] * world
         dist.all_gather_object(handles, mine, group=group)
     else:
         handles = [mine]
-    be.peer_attach(handles, rank, timeout_ms)
+    if ok and all(isinstance(h, bytes) and len(h) > 0 for h in handles):
+        try:
+            be.peer_attach(handles, rank, timeout_ms)
+        except Exception:  # noqa: BLE001
+            ok = False
+    else:
+        ok = False
     if world > 1:
         dist.barrier(group=group)
-    _ATTACHED[id(group)] = world
-    return True
+    if ok:
+        _ATTACHED[id(group)] = world
+    return ok
 
 
 def u64_to_i64(x: int) -> int:

@@ -163,6 +163,18 @@ def _worker(rank, world, port, q, tmpdir=None):
         out[("F4", 9, 9)] = D.stats(9, 9, backend=sim, device=cpu)
         out["epochs"] = sim.epoch
         D.detach_peers(backend=sim)
+        # a rank whose attach fails still completes the collectives; the
+        # ranks agree (MIN) and fall back to the NCCL/gloo all-reduce
+        class FailingSim(SlabSimBackend):
+            def peer_attach(self, handles, rank, timeout_ms):
+                raise RuntimeError("simulated IPC failure")
+        fb = FailingSim(tmpdir, rank) if rank == 1 else SlabSimBackend(tmpdir, rank)
+        ok = D.attach_peers(backend=fb)
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        out["attach_ok"] = (bool(ok), bool(t.item()))
+        D.detach_peers(backend=fb)
+        out["after_fail"] = D.stats(2, 10**5 + 1, backend=be, device=cpu)
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -180,6 +192,10 @@ def test_two_rank_gloo_stats_batch_and_wrap():
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
+    assert res[0]["attach_ok"] == (True, False) and res[1]["attach_ok"] == (False, False)
+    assert res[0]["after_fail"] == res[1]["after_fail"] == oracle.stats(2, 10**5 + 1)
+    for rr in res.values():
+        del rr["attach_ok"]
     assert res[0] == res[1]
     r = res[0]
     for key, val in r.items():
