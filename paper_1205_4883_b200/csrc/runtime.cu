@@ -1009,6 +1009,7 @@ void sieve_shutdown(void) {
   g.partials.release(); g.done.release(); g.result.release(); g.bitmap.release();
   g.list.release(); g.items.release(); g.bres.release();
   g.buckets.release(); g.kflags.release(); g.lflags.release(); g_f2.buf.release();
+  g.gbar.release(); g.bcounts.release();  // fused A2 (re-created, zeroed, on demand)
   peer_detach();
   g.peer.ptrs.release();
   if (g.peer.slab) cudaFree(g.peer.slab);

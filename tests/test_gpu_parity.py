@@ -360,3 +360,31 @@ def test_small_ranges_fused_sync_paths(lo, hi):
     assert c == oc and np.array_equal(bm[: obm.size], obm)
     lst, n = sv.primes(lo, hi)
     assert np.array_equal(lst[:n], oracle.primes(lo, hi))
+
+
+def test_lifecycle_shutdown_options_streams():
+    """Library state across calls: shutdown and re-initialisation (scratch,
+    tickets and grid-barrier counters re-created), option changes between
+    fused launches (segment size, wheel, threads), a user stream, and the
+    separate K1 path after the fused one -- every result against the oracle."""
+    torch = pytest.importorskip("torch")
+    want = oracle.stats(10**9, 10**9 + 10**7)
+    assert sv.stats(10**9, 10**9 + 10**7) == want
+    sv.shutdown()
+    assert sv.stats(10**9, 10**9 + 10**7) == want
+    for opts in [dict(segment_kb=32), dict(segment_kb=208, wheel=47 - 6), dict(threads=512),
+                 dict(segment_kb=96, wheel=17), dict()]:
+        sv.set_options(**opts)
+        assert sv.stats(10**9, 10**9 + 10**7) == want, opts
+        assert sv.stats(2, 10**6) == oracle.stats(2, 10**6), opts
+    st = torch.cuda.Stream()
+    sv.set_stream(st)
+    try:
+        assert sv.stats(10**9, 10**9 + 10**7) == want
+        lst, n = sv.primes(10**9, 10**9 + 10**5)
+        assert np.array_equal(lst[:n], oracle.primes(10**9, 10**9 + 10**5))
+    finally:
+        sv.set_stream(None)
+    sv.shutdown()
+    lst, n = sv.primes(2, 10**5)
+    assert np.array_equal(lst[:n], oracle.primes(2, 10**5))
