@@ -112,6 +112,25 @@ constexpr uint32_t kSmemAlign = 128;
 
 // launch bound of the sieve kernel (threads per CTA); the runtime never
 // launches more (sieve_options.threads is clamped to it)
+// default options (build-time overridable for same-box A/B variants)
+#ifndef SIEVE_DEFAULT_SEGMENT_KB
+#define SIEVE_DEFAULT_SEGMENT_KB 208
+#endif
+#ifndef SIEVE_DEFAULT_WHEEL
+#define SIEVE_DEFAULT_WHEEL 31
+#endif
+#ifndef SIEVE_TMA_STORE  // A7 bitmap write-back by cp.async.bulk (0: 128-bit st.global)
+#define SIEVE_TMA_STORE 1
+#endif
+#ifndef SIEVE_WB_DIAG  // diagnostics builds only: 1 = no wait for the bulk copy's reads, 2 = no bulk copy
+#define SIEVE_WB_DIAG 0
+#endif
+#ifndef SIEVE_UNTRANSPOSE_ILP  // blocks per warp and pass of the bit transpose
+#define SIEVE_UNTRANSPOSE_ILP 2
+#endif
+#ifndef SIEVE_WHEEL_UNROLL  // unroll of the wheel-init word loop (count mode)
+#define SIEVE_WHEEL_UNROLL 4
+#endif
 #ifndef SIEVE_MAX_THREADS
 #define SIEVE_MAX_THREADS 1024
 #endif

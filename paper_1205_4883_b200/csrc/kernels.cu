@@ -168,7 +168,9 @@ __device__ __forceinline__ void wheel_setup(uint32_t (&ig)[NG], uint32_t (&d4)[N
   }
 }
 
-template <int NG>
+// (count mode unrolls the word loop: SIEVE_WHEEL_UNROLL, same-box A/B)
+constexpr int kWheelUnroll = SIEVE_WHEEL_UNROLL;
+template <int NG, int UNR = 1>
 __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, uint64_t o0,
                                            uint64_t bit0, uint32_t valid, uint64_t a) {
   const uint32_t nt = blockDim.x, tid = threadIdx.x;
@@ -182,6 +184,7 @@ __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, u
   const uint32_t wfast_hi = (valid >> 10) << 5;
   uint32_t w = tid;
   if (wfast_lo == 0) {
+#pragma unroll UNR
     for (; w < wfast_hi; w += nt) seg[w] = wheel_word<0, NG>(tabb, ig, d4, e4);
   }
   for (; w < nwords; w += nt) {
@@ -682,6 +685,7 @@ __device__ __forceinline__ void bucket_drain(const SieveParams &P, uint32_t &cnt
 // its partner's columns c + w, so each lane sends itself rotated right by w
 // (upper partner) or 32 - w (lower partner) and merges with one bit-select:
 // three instructions (SHF, SHFL, LOP3) per stage.
+template <bool kInvert = false>
 __device__ __forceinline__ void untranspose(uint32_t *seg, uint32_t valid) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t nblk = (valid + 1023u) >> 10;
@@ -694,15 +698,52 @@ __device__ __forceinline__ void untranspose(uint32_t *seg, uint32_t valid) {
     amt[k] = (lane & w) ? 32u - w : w;
     keep[k] = (lane & w) ? ~m : m;
   }
-  for (uint32_t B = warp; B < nblk; B += nw) {
-    uint32_t x = seg[32u * B + lane];
+  // kUT independent blocks per warp and pass: the five shuffle stages of one
+  // block are a dependent chain (~200 cycles), interleaving hides it
+  constexpr int kUT = SIEVE_UNTRANSPOSE_ILP;
+  for (uint32_t B = warp; B < nblk; B += kUT * nw) {
+    uint32_t x[kUT];
+#pragma unroll
+    for (int u = 0; u < kUT; ++u) {
+      const uint32_t Bu = B + u * nw;
+      x[u] = Bu < nblk ? seg[32u * Bu + lane] : 0u;
+    }
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-      const uint32_t y = __shfl_xor_sync(0xffffffffu, __funnelshift_r(x, x, amt[k]), 16u >> k);
-      asm("lop3.b32 %0, %0, %1, %2, 0xE4;" : "+r"(x) : "r"(y), "r"(keep[k]));  // (x & keep) | (y & ~keep)
+#pragma unroll
+      for (int u = 0; u < kUT; ++u) {
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, __funnelshift_r(x[u], x[u], amt[k]), 16u >> k);
+        asm("lop3.b32 %0, %0, %1, %2, 0xE4;" : "+r"(x[u]) : "r"(y), "r"(keep[k]));  // (x & keep) | (y & ~keep)
+      }
     }
-    seg[32u * B + lane] = x;
+#pragma unroll
+    for (int u = 0; u < kUT; ++u) {
+      const uint32_t Bu = B + u * nw;
+      if (Bu < nblk) seg[32u * Bu + lane] = kInvert ? ~x[u] : x[u];
+    }
   }
+}
+
+// A7 by TMA (bitmap mode): the segment's words go from shared memory to HBM
+// as one bulk copy issued by one thread (cp.async.bulk, async proxy), so the
+// stores cost no instructions of the other threads and drain while they count.
+// The threads' generic-proxy writes are fenced to the async proxy before the
+// block barrier that precedes the copy; the issuing thread waits for the
+// copy's shared-memory reads before the buffer is reused.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+               "cp.async.bulk.commit_group;"
+               ::"l"(gdst), "r"((uint32_t)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // A6/A7: count, sum and (bitmap mode) write-back of one segment.
@@ -738,14 +779,25 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
   // planes of per-bit-position counts (counts < 512: <= 127 quads per thread)
   uint32_t ones = 0, twos = 0, fours = 0, p8 = 0, p16 = 0, p32 = 0, p64 = 0, p128 = 0;
   uint32_t C = 0, X = 0, Q = 0;  // count, sum of e c_e, sum of k c_k
+  // bitmap mode: seg holds the prime words (untranspose<true>); with a
+  // 16-byte aligned output the whole 16-byte prefix of the segment's words
+  // goes by one bulk copy (the call's last segment may end in < 4 words,
+  // stored below)
+  uint32_t n16 = 0;
+  if (MODE == kBitmap && SIEVE_TMA_STORE && vec4) {
+    const uint64_t nw = out_words > w0 ? min((uint64_t)4u * nq, out_words - w0) : 0ull;
+    n16 = (uint32_t)nw & ~3u;
+#if SIEVE_WB_DIAG != 2
+    if (threadIdx.x == 0 && n16) bulk_store(out + w0, seg, 4u * n16);
+#endif
+  }
   uint32_t k = 0;
   for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x, ++k) {
     const uint4 v = seg4[q];
     // count mode counts the composite (set) bits and converts at the end
     // (every statistic below is linear in the per-position counts); bitmap
-    // mode needs the prime words themselves for the stores
-    const uint32_t x0 = kNatural ? ~v.x : v.x, x1 = kNatural ? ~v.y : v.y;
-    const uint32_t x2 = kNatural ? ~v.z : v.z, x3 = kNatural ? ~v.w : v.w;
+    // mode holds the prime words themselves
+    const uint32_t x0 = v.x, x1 = v.y, x2 = v.z, x3 = v.w;
     const uint32_t c0 = __popc(x0), c1 = __popc(x1), c2 = __popc(x2), c3 = __popc(x3);
     const uint32_t cq = c0 + c1 + c2 + c3;
     C += cq;
@@ -764,7 +816,14 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
     p128 ^= cy;
     if (MODE == kBitmap) {
       const uint64_t gw = w0 + 4ull * q;
-      if (vec4 && gw + 4 <= out_words) {
+      if (SIEVE_TMA_STORE && vec4) {
+        if (4u * q >= n16) {  // past the bulk copy
+          if (gw < out_words) out[gw] = x0;
+          if (gw + 1 < out_words) out[gw + 1] = x1;
+          if (gw + 2 < out_words) out[gw + 2] = x2;
+          if (gw + 3 < out_words) out[gw + 3] = x3;
+        }
+      } else if (vec4 && gw + 4 <= out_words) {
         reinterpret_cast<uint4 *>(out)[gw >> 2] = make_uint4(x0, x1, x2, x3);
       } else {
         if (gw < out_words) out[gw] = x0;
@@ -790,6 +849,9 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
                               : Jq - 124ull * (threadIdx.x & 7u) * C + X + 32ull * Bs;
   cnt += C;
   sum += (unsigned long long)C * a + 2ull * J;
+#if SIEVE_WB_DIAG == 0
+  if (MODE == kBitmap && SIEVE_TMA_STORE && threadIdx.x == 0 && n16) bulk_wait_read();
+#endif
 }
 
 constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;  // look-back flag states (A2 K1, A8 list)
@@ -1266,6 +1328,7 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
 template <int NG, int MODE>
 __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
+  constexpr int kWheelUnrollOf = MODE == kCount ? kWheelUnroll : 1;
   // segment at the first 128-byte boundary of the dynamic shared memory (the
   // runtime allocates kSmemAlign spare bytes), wheel tables after it
   const uint32_t sraw = (uint32_t)__cvta_generic_to_shared(smem);
@@ -1310,8 +1373,8 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     base_phase(P, seg);
     if (pre_init) {
       const uint64_t bit0 = s_begin * (uint64_t)P.seg_bits, left = P.nbits - bit0;
-      wheel_init<NG>(seg, tab, P.o0, bit0, left < P.seg_bits ? (uint32_t)left : P.seg_bits,
-                     P.o0 + 2ull * bit0);
+      wheel_init<NG, kWheelUnrollOf>(seg, tab, P.o0, bit0, left < P.seg_bits ? (uint32_t)left : P.seg_bits,
+                                     P.o0 + 2ull * bit0);
     }
     grid_wait(P.gbar, 2u * gridDim.x);
     if (P.prof && threadIdx.x == 0) atomicMax(P.prof + 118, global_ns());
@@ -1366,7 +1429,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       a = o0 + 2ull * bit0;
     }
     const long long c0 = P.prof ? clock64() : 0;
-    if (!(pre_init && s == s_begin)) wheel_init<NG>(seg, tab, o0, bit0, valid, a);
+    if (!(pre_init && s == s_begin)) wheel_init<NG, kWheelUnrollOf>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
     if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);
@@ -1392,7 +1455,8 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       cnt += list_emit(seg, s, a, valid, P, s_wc, &s_off);
     } else {
       if (MODE == kBitmap) {
-        untranspose(seg, valid);
+        untranspose<true>(seg, valid);
+        if (SIEVE_TMA_STORE) fence_proxy_async_smem();
         __syncthreads();
       }
       epilogue<MODE>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
@@ -1407,6 +1471,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     }
   }
   if (MODE == kBatch) return;
+  if (MODE == kBitmap && SIEVE_TMA_STORE && threadIdx.x == 0) bulk_wait_all();
 
   // per-CTA partial added into the launch's accumulator (u64 atomics: exact
   // mod 2^64, so the order does not matter); the last CTA to finish takes

@@ -154,8 +154,8 @@ constexpr size_t kMaxDynSmem = 227 * 1024 - 1024;  // per-block limit minus stat
 
 void default_options(sieve_options &o) {
   memset(&o, 0, sizeof o);
-  o.segment_kb = 208;
-  o.wheel = 31;  // A/B with the skip of multiples of 3 and 5: 31 beats 41 by 1.4-1.8 %
+  o.segment_kb = SIEVE_DEFAULT_SEGMENT_KB;
+  o.wheel = SIEVE_DEFAULT_WHEEL;  // A/B with the skip of multiples of 3 and 5: 31 beats 41 by 1.4-1.8 %
   o.ctas_per_sm = 0;
   o.threads = SIEVE_MAX_THREADS;
 }

@@ -151,6 +151,34 @@ def test_primes_list_truncation_and_device_out():
     assert cb == oc and np.array_equal(db.cpu().numpy().view(np.uint32), obm)
 
 
+@pytest.mark.parametrize("shift", [0, 1, 2, 3])
+def test_bitmap_bulk_copy_edges(shift):
+    """A7 by TMA bulk copy (csrc/kernels.cu epilogue<kBitmap>): device outputs
+    at 4-byte offsets 0..3 words past a 16-byte boundary (0: the bulk copy;
+    else the 32-bit store path), ranges whose word count ends 0..3 words past
+    a 16-byte multiple (the last < 4 words go by plain stores) and spanning
+    several segments, and guard words before and after the output that must
+    stay untouched."""
+    torch = pytest.importorskip("torch")
+    sv.set_options(segment_kb=16)
+    try:
+        for k, lo in enumerate([10**9 + 1, 3, 10**12 + 7]):
+            for tail in range(4):
+                w = 4 * (997 + 13 * k) + tail + 32 * 4096   # several 16 KiB segments
+                hi = lo + 64 * w - (5 if lo % 2 else 6)     # last word partially valid
+                assert sv.bitmap_words(lo, hi) == w
+                buf = torch.full((w + 8,), -1, dtype=torch.int32, device="cuda")
+                out = buf[shift: shift + w]
+                _, cb = sv.bitmap(lo, hi, out=out)
+                obm, oc, _ = oracle.bitmap(lo, hi)
+                got = buf.cpu().numpy().view(np.uint32)
+                assert cb == oc, (lo, tail, shift)
+                assert np.array_equal(got[shift: shift + w], obm), (lo, tail, shift)
+                assert (got[:shift] == 0xFFFFFFFF).all() and (got[shift + w:] == 0xFFFFFFFF).all()
+    finally:
+        sv.set_options()
+
+
 def test_repeat_determinism():
     lo, hi = 2, 2 * 10**8 + 1
     a = [sv.stats(lo, hi) for _ in range(3)]
