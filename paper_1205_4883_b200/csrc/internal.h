@@ -122,7 +122,7 @@ constexpr uint32_t kSmemAlign = 128;
 #ifndef SIEVE_TMA_STORE  // A7 bitmap write-back by cp.async.bulk (0: 128-bit st.global)
 #define SIEVE_TMA_STORE 1
 #endif
-#ifndef SIEVE_WB_DIAG  // diagnostics builds only: 1 = no wait for the bulk copy's reads, 2 = no bulk copy
+#ifndef SIEVE_WB_DIAG  // diagnostics builds only: 1 = no wait for the bulk copy's reads, 2 = no bulk copy, 3 = no transpose
 #define SIEVE_WB_DIAG 0
 #endif
 #ifndef SIEVE_UNTRANSPOSE_ILP  // blocks per warp and pass of the bit transpose

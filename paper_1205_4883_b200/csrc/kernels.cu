@@ -1455,7 +1455,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       cnt += list_emit(seg, s, a, valid, P, s_wc, &s_off);
     } else {
       if (MODE == kBitmap) {
-        untranspose<true>(seg, valid);
+        if (SIEVE_WB_DIAG != 3) untranspose<true>(seg, valid);
         if (SIEVE_TMA_STORE) fence_proxy_async_smem();
         __syncthreads();
       }
