@@ -179,6 +179,38 @@ def test_bitmap_bulk_copy_edges(shift):
         sv.set_options()
 
 
+def test_managed_memory_outputs():
+    """Managed (unified) memory counts as device memory at the ABI
+    (runtime.cu is_device_ptr): the kernels write it directly -- the bitmap
+    by the TMA bulk copy, the list by its 16-byte stores -- and the host
+    reads it after the call."""
+    import ctypes
+    torch = pytest.importorskip("torch")
+    torch.cuda.init()
+    rt = ctypes.CDLL("/usr/local/cuda/lib64/libcudart.so.12")
+    lo, hi = 10**11 + 1, 10**11 + 3 * 10**6 + 2
+    w = sv.bitmap_words(lo, hi)
+    full = oracle.primes(lo, hi)
+    ptrs = []
+    try:
+        for nbytes in (4 * w, 8 * full.size):
+            p = ctypes.c_void_p()
+            assert rt.cudaMallocManaged(ctypes.byref(p), ctypes.c_size_t(nbytes), 1) == 0
+            ptrs.append(p.value)
+        L = sv.lib()
+        cb = L.sieve_bitmap(lo, hi, ptrs[0])
+        cl = L.sieve_primes(lo, hi, ptrs[1], full.size)
+        assert rt.cudaDeviceSynchronize() == 0
+        obm, oc, _ = oracle.bitmap(lo, hi)
+        got_bm = np.ctypeslib.as_array(ctypes.cast(ptrs[0], ctypes.POINTER(ctypes.c_uint32)), (w,)).copy()
+        got_l = np.ctypeslib.as_array(ctypes.cast(ptrs[1], ctypes.POINTER(ctypes.c_uint64)), (full.size,)).copy()
+        assert cb == oc and np.array_equal(got_bm, obm)
+        assert cl == full.size and np.array_equal(got_l, full)
+    finally:
+        for p in ptrs:
+            rt.cudaFree(ctypes.c_void_p(p))
+
+
 def test_repeat_determinism():
     lo, hi = 2, 2 * 10**8 + 1
     a = [sv.stats(lo, hi) for _ in range(3)]
