@@ -131,6 +131,9 @@ constexpr uint32_t kSmemAlign = 128;
 #ifndef SIEVE_WHEEL_UNROLL  // unroll of the wheel-init word loop (count mode)
 #define SIEVE_WHEEL_UNROLL 4
 #endif
+#ifndef SIEVE_EPI_PAIRS  // count/batch epilogue: two quads per carry-save step
+#define SIEVE_EPI_PAIRS 1
+#endif
 #ifndef SIEVE_MAX_THREADS
 #define SIEVE_MAX_THREADS 1024
 #endif

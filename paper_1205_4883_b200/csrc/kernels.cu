@@ -792,7 +792,34 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
 #endif
   }
   uint32_t k = 0;
-  for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x, ++k) {
+  uint32_t q = threadIdx.x;
+  if (!kNatural && SIEVE_EPI_PAIRS) {
+    // count/batch modes: two quads (8 words) per carry-save step, so the
+    // half-adder chain above weight 8 runs once per 8 words instead of 4
+    for (; q + blockDim.x < nq; q += 2u * blockDim.x, k += 2u) {
+      const uint4 v = seg4[q], u = seg4[q + blockDim.x];
+      const uint32_t c0 = __popc(v.x), c1 = __popc(v.y), c2 = __popc(v.z), c3 = __popc(v.w);
+      const uint32_t d0 = __popc(u.x), d1 = __popc(u.y), d2 = __popc(u.z), d3 = __popc(u.w);
+      const uint32_t cq = c0 + c1 + c2 + c3, dq = d0 + d1 + d2 + d3;
+      C += cq + dq;
+      Q += k * (cq + dq) + dq;  // quads k and k + 1
+      X += (c1 + d1) + 2u * (c2 + d2) + 3u * (c3 + d3);
+      uint32_t tA, tB, fA, tC, tD, fB, e;
+      csa(tA, ones, ones, v.x, v.y);
+      csa(tB, ones, ones, v.z, v.w);
+      csa(fA, twos, twos, tA, tB);
+      csa(tC, ones, ones, u.x, u.y);
+      csa(tD, ones, ones, u.z, u.w);
+      csa(fB, twos, twos, tC, tD);
+      csa(e, fours, fours, fA, fB);
+      uint32_t cz = p8 & e; p8 ^= e;
+      uint32_t cy = p16 & cz; p16 ^= cz;
+      cz = p32 & cy; p32 ^= cy;
+      cy = p64 & cz; p64 ^= cz;
+      p128 ^= cy;
+    }
+  }
+  for (; q < nq; q += blockDim.x, ++k) {
     const uint4 v = seg4[q];
     // count mode counts the composite (set) bits and converts at the end
     // (every statistic below is linear in the per-position counts); bitmap
