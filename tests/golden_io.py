@@ -45,3 +45,19 @@ def subwindows():
         s, c, sm, h = l.split()
         out.append((int(s), int(c), int(sm), int(h, 16)))
     return out
+
+
+def config3_blocks():
+    """tests/golden/config3_blocks.txt -> list of (G, g, lo, hi, count, sum)."""
+    return [tuple(int(t) for t in l.split()) for l in _lines("config3_blocks.txt")]
+
+
+def config5_oracle():
+    """tests/golden/config5_oracle.txt (written by tools/regen_golden.py from
+    oracle/ only) -> (lo, hi, count, sum) uint64 arrays in interval order."""
+    import numpy as np
+
+    rows = [l.split() for l in _lines("config5_oracle.txt")]
+    assert [int(r[0]) for r in rows] == list(range(len(rows)))
+    cols = [np.array([int(r[k]) for r in rows], dtype=np.uint64) for k in range(1, 5)]
+    return tuple(cols)

@@ -13,7 +13,7 @@ import inputs
 import oracle
 import paper_1205_4883_b200 as sv
 from paper_1205_4883_b200.dist import block_of
-from golden_io import kv, subwindows
+from golden_io import config3_blocks, config5_oracle, kv, subwindows
 from independent import is_prime_td
 
 pytestmark = pytest.mark.gpu
@@ -249,9 +249,11 @@ def test_config3_count_sum_and_blocks():
             tot_c += c
             tot_s = (tot_s + s) & MASK64
         assert (tot_c, tot_s) == (int(PINS["config3.count"]), int(PINS["config3.sum"]))
-    # G=2 block values pinned in SURVEY.md 8(c) C3
-    assert sv.stats(2, 5000000003) == (234954223, 572840944428163514)
-    assert sv.stats(5000000003, 10000000001) == (220098288, 1647981488153565724)
+    # every block of G = 2, 4, 8 against tests/golden/config3_blocks.txt
+    # (reproduced by the oracle in test_oracle_golden.py)
+    for G, g, a, b, c, s in config3_blocks():
+        assert block_of(lo, hi, g, G) == (a, b)
+        assert sv.stats(a, b) == (c, s), (G, g)
 
 
 # ---------------------------------------------------------------- config 4
@@ -281,6 +283,11 @@ def test_config5_batch_digest_and_samples():
     assert int(c.sum()) == int(PINS["config5.count_total"])
     assert int(s.sum(dtype=np.uint64)) == int(PINS["config5.sum_total"])
     assert oracle.fnv1a64(inter) == int(PINS["config5.digest"], 16)
+    # every interval element-wise against the oracle's values
+    # (tests/golden/config5_oracle.txt, written by tools/regen_golden.py)
+    flo, fhi, fc, fs = config5_oracle()
+    assert np.array_equal(lo, flo) and np.array_equal(hi, fhi)
+    assert np.array_equal(c, fc) and np.array_equal(s, fs)
     idx = np.array([0, 1, 2, 3, 4095] + list(range(7, 4096, 409)))
     oc, os_ = oracle.batch(lo[idx], hi[idx])
     assert np.array_equal(c[idx], oc) and np.array_equal(s[idx], os_)
