@@ -40,8 +40,8 @@ UNIT = "integers/s"
 CONFIG3 = (2, 10**10 + 1)
 PI_1E10 = 455052511                  # BASELINE.json north_star
 SUM_1E10 = 2220822432581729238       # SURVEY.md 8(c) C3 (Lucy-Hedgehog)
-WHEEL_ALG = 19                       # M_alg is defined with wheel bound 19
-SMEM_LANES_PER_CLK = 32              # one conflict-free shared-memory wavefront / clk / SM
+WHEEL_BASELINE_MD = 19               # BASELINE.md 4 quotes M_alg with wheel bound 19 (secondary field)
+SMEM_LANES_PER_CLK_NOMINAL = 32      # one shared-memory wavefront / clk / SM (fallback if K0 fails)
 
 
 def parse():
@@ -62,10 +62,13 @@ def parse():
                          "memory (F4, csrc/peer.cuh; falls back to nccl on every rank if any rank "
                          "cannot attach or verify it) or a separate NCCL all-reduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=4 * 10**9,
-                    help="integers of config 3 the oracle sieves for cpu_baseline")
-    ap.add_argument("--ref-sample", type=int, default=4 * 10**8,
-                    help="integers per --impl reference step")
+    ap.add_argument("--cpu-sample", type=int, default=10**10 - 1,
+                    help="integers of config 3 the oracle sieves for cpu_baseline (default: all)")
+    ap.add_argument("--cpu-sample-t1", type=int, default=10**9,
+                    help="integers of config 3 the single-thread oracle run sieves")
+    ap.add_argument("--ref-budget-s", type=float, default=200.0,
+                    help="--impl reference: the K timed steps take about this long in all; each step "
+                         "is the whole config-3 range when that fits, else an equal prefix sample")
     return ap.parse_args()
 
 
@@ -138,10 +141,11 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- roofline
-def algorithmic_marks(lo: int, hi: int, wheel: int = WHEEL_ALG) -> int:
+def algorithmic_marks(lo: int, hi: int, wheel: int) -> int:
     """M_alg: number of (odd prime p, odd multiple m) pairs with wheel < p <=
     isqrt(hi-1) and max(lo, p^2) <= m < hi -- the marks the method must make
-    beyond the wheel."""
+    beyond the wheel bound the build uses ("M_alg is the
+    exact mark count ... for the wheel bound the build uses")."""
     import numpy as np
     if hi <= lo or hi < 10:
         return 0
@@ -164,15 +168,15 @@ def algorithmic_marks(lo: int, hi: int, wheel: int = WHEEL_ALG) -> int:
     return total
 
 
-def load_traffic():
-    """dram bytes per launch of the sieve kernel from the committed ncu capture."""
+def load_ncu_summary() -> dict:
+    """Per-launch counters of the sieve kernel from the committed ncu capture
+    (tools/make_profile_summary.py): DRAM traffic and the hardware view."""
     path = os.path.join(ROOT, "profiles", "ncu_sieve_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch")
+            return json.load(f)
     except Exception:  # noqa: BLE001
-        return None
+        return {}
 
 
 def load_peaks():
@@ -184,31 +188,59 @@ def load_peaks():
 
 
 # ----------------------------------------------------------------- reference arm
+def host_cpu() -> dict:
+    """The host the oracle runs on: logical CPUs (nproc) and model name."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
     import oracle
-    lo = CONFIG3[0]
-    n = min(args.ref_sample, CONFIG3[1] - lo)
+    lo, hi = CONFIG3
     cores = oracle.default_threads()
-    for _ in range(args.warmup):
-        oracle.stats(lo, lo + min(n, 10**7), cores)
+    # warm-up steps on a 10^9 prefix, which also measures the oracle's rate;
+    # each timed step is then the whole range if K of them fit the budget,
+    # else an equal prefix sample sized to it (stated in config/cpu_baseline)
+    rate = None
+    for _ in range(max(args.warmup, 1)):
+        t0 = time.perf_counter()
+        oracle.stats(lo, lo + 10**9, cores)
+        rate = 10**9 / (time.perf_counter() - t0)
+    n = hi - lo
+    if n / rate * args.steps > args.ref_budget_s:
+        n = max(10**8, int(rate * args.ref_budget_s / args.steps) // 10**8 * 10**8)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.stats(lo, lo + n, cores)
+        c, s = oracle.stats(lo, lo + n, cores)
         times.append(time.perf_counter() - t0)
     per = sum(times) / len(times)
     value = n / per
-    sample = f"[2, {lo + n}) of config 3 ({n} integers) per step, count+sum, {cores} threads"
+    full = n == hi - lo
+    if full:
+        assert (c, s) == (PI_1E10, SUM_1E10), (c, s)
+    sample = (f"[2, {lo + n}) of config 3 ({n} integers, "
+              f"{'the whole range' if full else 'prefix sample'}) per step, count+sum, {cores} threads")
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic", "config": {"workload": "config3: pi(1e10) count+sum (oracle sample)",
-                                        "sample_integers": n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": sample},
+        "data": "synthetic",
+        "config": {"workload": "config3: pi(1e10) count + prime sum over [2, 1e10+1)"
+                               + ("" if full else " (oracle prefix sample)"),
+                   "lo": lo, "hi": lo + n, "sample_integers": n, "same_config": full},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "threads": cores,
+                         "kind": "oracle", "sample": sample, **host_cpu()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -216,16 +248,29 @@ def run_reference(args, rank, world):
 
 
 def cpu_baseline(args):
+    """The oracle (never tuned) on the host cores: the whole config-3 range
+    with all hardware threads, and a single-thread run on a prefix sample."""
     import oracle
     cores = oracle.default_threads()
-    lo = CONFIG3[0]
-    n = min(args.cpu_sample, CONFIG3[1] - lo)
+    lo, hi = CONFIG3
+    n = min(args.cpu_sample, hi - lo)
     t0 = time.perf_counter()
-    oracle.stats(lo, lo + n, cores)
+    c, s = oracle.stats(lo, lo + n, cores)
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"[2, {lo + n}) = first {n} integers of config 3, count+sum, one run, "
-                      f"{dt:.2f} s"}
+    whole = n == hi - lo
+    out = {"value": n / dt, "unit": UNIT, "cores": cores, "threads": cores, "kind": "oracle",
+           "sample": (f"[2, {lo + n}) = " + ("the whole config-3 range" if whole else
+                                             f"first {n} integers of config 3")
+                      + f", count+sum, one run, {dt:.2f} s, {cores} threads"),
+           "verified": (c, s) == (PI_1E10, SUM_1E10) if whole else None, **host_cpu()}
+    n1 = min(args.cpu_sample_t1, hi - lo)
+    if n1 > 0:
+        t0 = time.perf_counter()
+        oracle.stats(lo, lo + n1, 1)
+        d1 = time.perf_counter() - t0
+        out["t1"] = {"value": n1 / d1, "unit": UNIT, "threads": 1,
+                     "sample": f"[2, {lo + n1}) = first {n1} integers of config 3, one run, {d1:.2f} s"}
+    return out
 
 
 # ----------------------------------------------------------------- our arm
@@ -315,6 +360,13 @@ def main():
         got = [D.i64_to_u64(x) for x in result.cpu().tolist()]
         verified = (got[0] == PI_1E10 and got[1] == SUM_1E10)
 
+    # K0: the conflict-free shared atomicOr rate of this
+    # GPU, measured in this run, outside the timed region
+    try:
+        k0_lanes, k0_ghz = sv.debug_k0()
+    except Exception as e:  # noqa: BLE001
+        print(f"rank {rank}: K0 failed ({e}); nominal 32 lanes/clk", file=sys.stderr)
+        k0_lanes, k0_ghz = None, None
     launches0 = sv.kernel_launches()
     sampler = ClockSampler(local)
     if world > 1:
@@ -372,17 +424,29 @@ def main():
         clocks = sampler.summary()
         peaks = load_peaks()
         sm_max = peaks.get("sm_max_mhz") or clocks.get("sm_max_mhz") or 1965.0
-        # whole-job marks / max-over-ranks kernel time, against
-        # N x the per-GPU peak (at N=1: the one launch)
-        m_alg = algorithmic_marks(lo, hi)
+        f_sm = clocks.get("sm_mhz") or sm_max  # the measured clock under load (D2 f_SM)
+        r_atom = k0_lanes if k0_lanes else SMEM_LANES_PER_CLK_NOMINAL
+        w = opts["wheel"]
+        # whole-job marks beyond the build's wheel /
+        # max-over-ranks kernel time, against N x 148 x R_atom (K0) x f_SM
+        m_alg = algorithmic_marks(lo, hi, w)
         achieved = m_alg / (sieve_ms_mean / 1e3) / 1e9
-        peak = world * 148 * SMEM_LANES_PER_CLK * sm_max * 1e6 / 1e9
+        peak = world * 148 * r_atom * f_sm * 1e6 / 1e9
+        ncu = load_ncu_summary()
+        m19 = algorithmic_marks(lo, hi, WHEEL_BASELINE_MD)
         roof = {"bound": "smem_atomic", "achieved": achieved, "peak": peak, "unit": "Gmarks/s",
-                "frac": achieved / peak, "traffic": load_traffic(),
+                "frac": achieved / peak, "traffic": ncu.get("dram_bytes_per_launch"),
                 "kernel": "sv::k_sieve<NG,kCount>" + ("" if bcast else " (A2 fused)"),
-                "marks_alg_per_launch": algorithmic_marks(a, b), "marks_alg_job": m_alg,
-                "peak_basis": f"{world} x 148 SMs x {SMEM_LANES_PER_CLK} shared-memory lanes/clk x "
-                              f"{sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
+                "wheel": w, "marks_alg_per_launch": algorithmic_marks(a, b, w), "marks_alg_job": m_alg,
+                "peak_basis": (f"{world} x 148 SMs x R_atom {r_atom:.3f} lanes/clk (K0 in this run"
+                               + ("" if k0_lanes else ": failed, nominal 32") + f") x f_SM {f_sm:.0f} MHz "
+                               "(median SM clock sampled during the timed steps)"),
+                "k0": {"lanes_per_clk_per_sm": k0_lanes, "sm_ghz": k0_ghz},
+                "w19": {"marks_alg_job": m19, "frac": m19 / (sieve_ms_mean / 1e3) / 1e9 / peak,
+                        "note": "M_alg with the wheel bound 19 of BASELINE.md 4 (context only)"},
+                "hw": {k: ncu.get(k) for k in ("atomic_lane_util", "lane_atomics_per_launch",
+                                                "smem_pipe_pct", "atomic_wavefronts_per_instr",
+                                                "issue_active_pct", "tag")},
                 "kernel_ms": sieve_ms_mean, "kernel_share_of_step": sieve_ms_mean / ms_per_step}
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -402,9 +466,11 @@ def main():
             "roofline": roof,
             "clocks": clocks,
             "gpu_launches": launches,
-            "e2e": {"value": (hi - lo) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16,
+            "e2e": {"value": (hi - lo) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 16, "ms_per_step": e2e_s * 1e3,
-                    "api": "sieve_stats (host outputs)" if world == 1 else "dist.stats"},
+                    "api": "sieve_stats (host outputs)" if world == 1 else "dist.stats",
+                    "inputs": "lo, hi travel as kernel parameters (no input buffer to copy); the "
+                              "result (count, sum) is read back to the host every step"},
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)

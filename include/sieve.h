@@ -112,6 +112,18 @@ int sieve_batch(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t *co
 /* library stream and return without synchronizing.                        */
 /* ---------------------------------------------------------------------- */
 
+/* Batch mode on device-resident intervals (config 5; what sieve_batch runs
+ * after copying its host arrays): lo[i], hi[i] for i < n (device uint64),
+ * result[2i] = count and result[2i+1] = sum mod 2^64 of [lo[i], hi[i])
+ * (device, 2n uint64, overwritten).  hi_max >= every hi[i] (bounds the base
+ * primes, <= 2^48) and width_max >= every hi[i] - lo[i] (bounds the items
+ * per interval) are promises of the caller: an interval longer than
+ * width_max gets the sentinel (2^64-1, 2^64-1); hi[i] > hi_max gives wrong
+ * results.  lo[i] <= hi[i] is required.  The plan (items of at most one
+ * segment, costliest first) is made on the device: no host pass. */
+int sieve_batch_async(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t hi_max,
+                      uint64_t width_max, uint64_t *result);
+
 /* Upper bound on the number of odd primes <= r (sizes base-prime buffers). */
 uint64_t sieve_base_capacity(uint64_t r);
 
@@ -150,10 +162,19 @@ int sieve_stats_base_async(uint64_t lo, uint64_t hi, uint32_t *primes, uint64_t 
 int sieve_bitmap_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const uint64_t *recips,
                        const uint32_t *nbase, uint32_t *out, uint64_t *result);
 
+/* Bitmap mode with the base primes computed in the same launch (fused A2,
+ * as sieve_stats_base_async; cap >= sieve_base_capacity(isqrt(hi-1))):
+ * writes sieve_bitmap_words(lo,hi) words into out (device, any 4-byte
+ * alignment) and result[0..1] = (count, sum mod 2^64) -- what sieve_bitmap
+ * does, without the host round trip. */
+int sieve_bitmap_base_async(uint64_t lo, uint64_t hi, uint32_t *primes, uint64_t *recips,
+                            uint32_t *nbase, uint64_t cap, uint32_t *out, uint64_t *result);
+
 /* ---------------------------------------------------------------------- */
-/* the gather of the paper's flow (PAPER.md:163-169,    */
-/* Fig. 6 -- every node's result collected after its sieve) for the        */
-/* count/sum path, fused into the sieve kernel: its last CTA writes this   */
+/* SURVEY.md 8(f) F4 (overlap: the collective fused into the kernel,      */
+/* PAPER.md:105-111) applied to the one exchange of the multi-GPU count    */
+/* path, the all-reduce of A9 that ends the paper's flow (PAPER.md:163-169 */
+/* "gather"): the sieve kernel's last CTA writes this                      */
 /* rank's (count, sum) into every peer's slab over NVLink (P2P stores of   */
 /* CUDA-IPC-mapped memory) and sums the slots the peers wrote into its own  */
 /* -- no separate collective launch.  One process per GPU; the calls below */
@@ -188,6 +209,15 @@ int sieve_peer_detach(void);
 /* Number of fused launches since the last attach (launch e uses slab
  * parity e & 1; slot layout in csrc/peer.cuh). */
 uint64_t sieve_peer_epoch(void);
+
+/* Publishes this rank's (count, sum) for the NEXT fused epoch into every
+ * attached slab and returns without waiting for the peers (the epoch
+ * advances as for a fused launch).  Lets a test run the ranks' kernels one
+ * after another on a single GPU -- rank 1 publishes, then rank 0's fused
+ * launch finds rank 1's share already there -- so that no two kernels ever
+ * wait on each other (B200_PROFILING.md: such kernels on one GPU are not
+ * guaranteed to run concurrently).  SIEVE_EINVAL when nothing is attached. */
+int sieve_peer_publish_async(uint64_t count, uint64_t sum);
 
 /* As sieve_stats_async on this rank's [lo, hi), then result[0..1] = the
  * sums over all attached ranks of their (count, sum mod 2^64).  A rank
@@ -227,8 +257,34 @@ int sieve_debug_set_profile(uint64_t *dev_counters);
 
 /* Diagnostics: flags for later launches.  1 = skip the marking step (A4/A5):
  * wheel init + count/write-back only, to time the bitmap write-back stage in
- * isolation.  Results are WRONG while set; 0 restores. */
+ * isolation; 2 / 4 / 8 = skip the marking regions (A1+A2) /
+ * (B) / (C) (marginal cost of a region).  Results are WRONG while any of
+ * these is set.  16 = every CTA walks its segments in reverse order (bitmap
+ * mode; schedule invariance: results must not change); 32 = never use the cooperative fused-A2 launch (the K1 + ordinary
+ * launch path the library falls back to when a cooperative launch is
+ * refused; results must not change).  0 restores. */
 int sieve_debug_set_flags(uint32_t flags);
+
+/* Diagnostics (bounds-check build, `make check` -> libsieve_check.so,
+ * compiled with -DSIEVE_CHECK_BOUNDS=1): out[0..3] = counts of
+ * shared-memory marks outside the CTA's segment words, bitmap stores outside
+ * out[0, words), list stores outside list[0, cap), and scratch writes
+ * (segment init/transpose, bucket rings, fused-A2 staging) outside their
+ * capacity, since load or the last reset (reset != 0 zeroes them after
+ * reading).  Synchronizes the library stream.  Returns 1 in the
+ * bounds-check build, 0 in the product build (where nothing is checked and
+ * the counts stay 0), < 0 on error. */
+int sieve_debug_violations(uint64_t *out, int reset);
+
+/* Diagnostics (K0): the conflict-free shared-memory
+ * atomicOr rate of this GPU, in lanes per SM-clock per SM (~32 on B200),
+ * and the SM clock the measurement ran at (GHz).  Runs a microbenchmark of
+ * three launches on the current device; synchronous. */
+int sieve_debug_k0(double *lanes_per_clk_per_sm, double *sm_ghz);
+
+/* Diagnostics: cooperative (fused-A2) launches that were refused and re-run
+ * as K1 + an ordinary launch, since load. */
+uint64_t sieve_debug_coop_fallbacks(void);
 
 /* ---------------------------------------------------------------------- */
 /* the paper's second algorithm pair, batched on the    */

@@ -79,9 +79,22 @@ def lib():
             "sieve_peer_epoch": (_u64, []),
             "sieve_stats_allreduce_async": (ctypes.c_int, [_u64, _u64, _p, _p, _p, _p]),
             "sieve_stats_base_async": (ctypes.c_int, [_u64, _u64, _p, _p, _p, _u64, ctypes.c_int, _p]),
+            "sieve_peer_publish_async": (ctypes.c_int, [_u64, _u64]),
+            "sieve_batch_async": (ctypes.c_int, [_p, _p, _u64, _u64, _u64, _p]),
+            "sieve_bitmap_base_async": (ctypes.c_int, [_u64, _u64, _p, _p, _p, _u64, _p, _p]),
+            "sieve_debug_violations": (ctypes.c_int, [_p, ctypes.c_int]),
+            "sieve_debug_k0": (ctypes.c_int, [_p, _p]),
+            "sieve_debug_coop_fallbacks": (_u64, []),
         }
         for name, (res, args) in sig.items():
-            f = getattr(L, name)
+            try:
+                f = getattr(L, name)
+            except AttributeError:
+                # an older variant build (SIEVE_LIBRARY, A/B runs) may lack a
+                # newer entry point; calling it then raises AttributeError
+                if library_path == os.path.join(_HERE, "libsieve.so"):
+                    raise
+                continue
             f.restype = res
             f.argtypes = args
         _lib = L
@@ -102,6 +115,19 @@ def _ptr(x) -> int | None:
     return x.data_ptr()  # torch tensor
 
 
+def _check_out(out, need: int, itemsize: int, what: str) -> None:
+    """An output buffer must hold `need` elements of `itemsize` bytes (numpy
+    array or torch tensor, contiguous): the C side writes exactly that many."""
+    if hasattr(out, "element_size"):  # torch
+        n, isz, contig = out.numel(), out.element_size(), out.is_contiguous()
+    else:
+        n, isz, contig = out.size, out.itemsize, out.flags["C_CONTIGUOUS"]
+    if isz != itemsize or not contig:
+        raise ValueError(f"{what}: need a contiguous buffer of {itemsize}-byte elements")
+    if n < need:
+        raise ValueError(f"{what}: buffer holds {n} elements, the call writes {need}")
+
+
 # ---- north_star calls -----------------------------------------------------
 def count(lo: int, hi: int) -> int:
     """Number of primes in [lo, hi)."""
@@ -119,6 +145,8 @@ def bitmap(lo: int, hi: int, out=None):
     w = bitmap_words(lo, hi)
     if out is None:
         out = np.zeros(max(w, 1), dtype=np.uint32)
+    elif w:
+        _check_out(out, w, 4, "bitmap out")
     c = _check(lib().sieve_bitmap(lo, hi, _ptr(out) if w else None))
     return out, c
 
@@ -129,6 +157,8 @@ def primes(lo: int, hi: int, cap: int | None = None, out=None):
         cap = count(lo, hi) if out is None else int(out.numel() if hasattr(out, "numel") else out.size)
     if out is None:
         out = np.zeros(max(cap, 1), dtype=np.uint64)
+    elif cap:
+        _check_out(out, cap, 8, "primes out")
     c = _check(lib().sieve_primes(lo, hi, _ptr(out) if cap else None, cap))
     return out, c
 
@@ -180,6 +210,24 @@ def stats_base_async(lo: int, hi: int, primes_t, recips_t, nbase_t, result_t,
                                         primes_t.numel(), 1 if allreduce else 0, _ptr(result_t)))
 
 
+def batch_async(lo_t, hi_t, hi_max: int, width_max: int, result_t) -> None:
+    """Batch mode on device tensors (int64 views of the uint64 bounds):
+    result_t[2i], result_t[2i+1] = count, sum mod 2^64 of [lo_t[i], hi_t[i])."""
+    n = int(lo_t.numel())
+    if hi_t.numel() != n or result_t.numel() < 2 * n:
+        raise ValueError("batch_async: lo/hi of equal length and result of 2n entries")
+    _check(lib().sieve_batch_async(_ptr(lo_t), _ptr(hi_t), n, hi_max, width_max, _ptr(result_t)))
+
+
+def bitmap_base_async(lo: int, hi: int, primes_t, recips_t, nbase_t, out_t, result_t) -> None:
+    """Base primes + bitmap of [lo, hi) in one launch; result_t = (count, sum)."""
+    w = bitmap_words(lo, hi)
+    if w:
+        _check_out(out_t, w, 4, "bitmap out")
+    _check(lib().sieve_bitmap_base_async(lo, hi, _ptr(primes_t), _ptr(recips_t), _ptr(nbase_t),
+                                         primes_t.numel(), _ptr(out_t), _ptr(result_t)))
+
+
 def bitmap_async(lo: int, hi: int, primes_t, recips_t, nbase_t, out_t, result_t) -> None:
     _check(lib().sieve_bitmap_async(lo, hi, _ptr(primes_t), _ptr(recips_t), _ptr(nbase_t),
                                     _ptr(out_t), _ptr(result_t)))
@@ -218,6 +266,11 @@ def peer_detach() -> None:
 
 def peer_epoch() -> int:
     return int(lib().sieve_peer_epoch())
+
+
+def peer_publish_async(count: int, sum_: int) -> None:
+    """Publish this rank's (count, sum) for the next fused epoch, no wait."""
+    _check(lib().sieve_peer_publish_async(count & ((1 << 64) - 1), sum_ & ((1 << 64) - 1)))
 
 
 def stats_allreduce_async(lo: int, hi: int, primes_t, recips_t, nbase_t, result_t) -> None:
@@ -312,3 +365,26 @@ def debug_set_flags(flags: int) -> None:
 
 def kernel_launches() -> int:
     return int(lib().sieve_kernel_launches())
+
+
+FLAG_SKIP_MARKING, FLAG_SKIP_A, FLAG_SKIP_B, FLAG_SKIP_C = 1, 2, 4, 8
+FLAG_REVERSE, FLAG_NO_COOP = 16, 32
+
+
+def debug_violations(reset: bool = False) -> tuple[bool, list[int]]:
+    """(is the bounds-check build, [smem marks, bitmap stores, list stores,
+    scratch writes] out of bounds since load / the last reset)."""
+    out = np.zeros(4, dtype=np.uint64)
+    rc = _check(lib().sieve_debug_violations(out.ctypes.data, 1 if reset else 0))
+    return rc == 1, [int(x) for x in out]
+
+
+def debug_k0() -> tuple[float, float]:
+    """K0: conflict-free shared atomicOr lanes per SM-clock per SM, and the SM GHz."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(lib().sieve_debug_k0(ctypes.addressof(a), ctypes.addressof(b)))
+    return a.value, b.value
+
+
+def debug_coop_fallbacks() -> int:
+    return int(lib().sieve_debug_coop_fallbacks())

@@ -137,6 +137,17 @@ constexpr uint32_t kSmemAlign = 128;
 #ifndef SIEVE_MAX_THREADS
 #define SIEVE_MAX_THREADS 1024
 #endif
+// Bounds-check build (make check -> libsieve_check.so; "no worker
+// writes outside its segment's bitmap ... ownership checks in debug builds"):
+// every shared-memory mark outside the CTA's segment words, every global
+// store outside its output array and every scratch write outside its
+// capacity is counted (never trapped) in a device counter per class, read by
+// sieve_debug_violations().  0 on the product build: the checks compile out.
+#ifndef SIEVE_CHECK_BOUNDS
+#define SIEVE_CHECK_BOUNDS 0
+#endif
+enum ViolationClass { kVioSmemMark = 0, kVioBitmapStore = 1, kVioListStore = 2, kVioScratch = 3,
+                      kVioClasses = 4 };
 
 // One work item of the batch kernel (step A10): one segment of one interval.
 struct BatchItem {
@@ -144,7 +155,7 @@ struct BatchItem {
   uint32_t valid;     // odd slots in the segment (<= segment bits)
   uint32_t interval;  // index of the interval (result slot)
   uint32_t r;         // isqrt(hi_interval - 1): marking primes p <= r
-  uint32_t nend;      // index of the first base prime > r (k_item_ends)
+  uint32_t nend;      // index of the first base prime > r (k_plan_emit)
 };
 
 struct SieveParams {
@@ -200,6 +211,7 @@ struct SieveParams {
   uint32_t rs;          // isqrt(r)
   uint32_t *bcounts;    // [gridDim.x] per-CTA prime counts, then [7] region boundaries
   unsigned int *gbar;   // grid barrier counter: 0 at launch, reset by the last CTA
+  const uint32_t *nitems;  // batch mode, device-planned: the item count (overrides nseg)
 };
 
 // Diagnostic flag: skip step A4/A5 (wheel init + count/write-back only), to
@@ -209,6 +221,13 @@ constexpr uint32_t kFlagSkipMarking = 1u;
 // Diagnostic flags: skip marking regions (A1+A2), (B), (C) -- marginal cost
 // of each region in context.  Wrong results by design.
 constexpr uint32_t kFlagSkipA = 2u, kFlagSkipB = 4u, kFlagSkipC = 8u;
+// Diagnostic flag (bitmap mode): every CTA walks its segments in the reverse
+// order (segment nseg-1-s instead of s) -- the schedule invariance of
+// SPEC.md:152-154; bitmap, count and sum must be identical.
+constexpr uint32_t kFlagReverse = 16u;
+// Diagnostic flag: never take the cooperative (fused A2) launch -- the path
+// the runtime falls back to when a cooperative launch is refused.
+constexpr uint32_t kFlagNoCoop = 32u;
 
 enum Mode { kCount = 0, kBitmap = 1, kBatch = 2, kList = 3 };
 
@@ -225,13 +244,24 @@ cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64
 uint32_t base_slices(uint32_t r);  // look-back flags the base-prime kernel needs
 cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
                            uint32_t cap, cudaStream_t s);
-cudaError_t launch_item_ends(BatchItem *items, uint64_t n, const uint32_t *primes,
-                             const uint32_t *nbase, cudaStream_t s);
+// A10 planning on the device (no host pass over the intervals): interval i
+// of B_i odd slots becomes k_i = ceil(B_i / S) equal items (an interval with
+// hi - lo > width_max gets the sentinel result 2^64-1 instead), items ordered by a
+// counting sort on a log2 cost class, largest first (cost = the slots plus
+// one first-hit reduction per base prime <= r_i, as the host planner had);
+// result[2i..2i+1] initialised with (1, 2) when 2 is in the interval, else 0.
+// scratch: hist/cursor [2 x kPlanBuckets] u32, per-interval [2 x n] u32,
+// *nitems.  The base primes <= isqrt(hi_max - 1) must be in primes/nbase.
+constexpr uint32_t kPlanBuckets = 256;
+cudaError_t launch_batch_plan(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint32_t S,
+                              uint64_t width_max, const uint32_t *primes, const uint32_t *nbase,
+                              uint32_t *scratch, BatchItem *items, uint32_t *nitems,
+                              uint64_t *result, cudaStream_t s);
 // peer.cu: the fused all-reduce alone, for a rank whose
 // block holds no odd slot (it still publishes, the peers wait for it)
 cudaError_t launch_peer_only(unsigned long long *const *peers, uint32_t world, uint32_t rank,
                              uint64_t epoch, uint64_t timeout_ns, uint64_t count, uint64_t sum,
-                             uint64_t *result, cudaStream_t s);
+                             uint64_t *result, cudaStream_t s, bool wait = true);
 // primality.cu (Alg. 2, Alg. 3, deterministic Miller-Rabin)
 cudaError_t launch_modpow(const uint64_t *a, const uint64_t *b, const uint64_t *c, uint64_t n,
                           uint64_t *out, cudaStream_t s);
@@ -239,5 +269,11 @@ cudaError_t launch_fermat(const uint64_t *p, uint64_t n, const uint64_t *draws, 
                           uint8_t *out, cudaStream_t s);
 cudaError_t launch_is_prime(const uint64_t *nums, uint64_t n, uint8_t *out, cudaStream_t s);
 int sieve_max_ctas_per_sm(int ng, int mode, int threads, size_t smem);
+// bounds-check build: violations per ViolationClass since the last reset
+// (all zero, and reset a no-op, in the product build)
+cudaError_t read_violations(unsigned long long *out, bool reset);
+// K0 (diagnostics): conflict-free shared-memory atomicOr
+// lanes per SM-clock per SM, measured on the device the library runs on
+cudaError_t k0_smem_atomic_rate(int nsm, double *lanes_per_clk_per_sm, double *sm_ghz);
 
 }  // namespace sv

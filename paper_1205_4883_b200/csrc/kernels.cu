@@ -33,6 +33,24 @@ namespace sv {
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 // ---------------------------------------------------------------------------
+// Bounds-check build (internal.h SIEVE_CHECK_BOUNDS): violations are counted
+// per class, never trapped; the product build compiles every check out.
+// ---------------------------------------------------------------------------
+__device__ unsigned long long g_violations[kVioClasses];
+#if SIEVE_CHECK_BOUNDS
+// the CTA's segment words in the shared window: [s_chk_lo, s_chk_hi) bytes
+__shared__ uint32_t s_chk_lo, s_chk_hi;
+#define SV_CHECK(cond, cls)                                             \
+  do {                                                                  \
+    if (!(cond)) atomicAdd(&g_violations[cls], 1ull);                   \
+  } while (0)
+#else
+#define SV_CHECK(cond, cls) \
+  do {                      \
+  } while (0)
+#endif
+
+// ---------------------------------------------------------------------------
 // helpers
 // ---------------------------------------------------------------------------
 // Offset (in odd slots from a) of the first odd multiple m of p with
@@ -104,6 +122,9 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // byte address: the segment base is 128-byte aligned and kept in a register,
 // so that the address arithmetic below needs no generic->shared conversion
 __device__ __forceinline__ void red_or(uint32_t saddr, uint32_t mask) {
+#if SIEVE_CHECK_BOUNDS
+  SV_CHECK(saddr >= s_chk_lo && saddr < s_chk_hi && __popc(mask) == 1, kVioSmemMark);
+#endif
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(saddr), "r"(mask) : "memory");
 }
 
@@ -185,7 +206,10 @@ __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, u
   uint32_t w = tid;
   if (wfast_lo == 0) {
 #pragma unroll UNR
-    for (; w < wfast_hi; w += nt) seg[w] = wheel_word<0, NG>(tabb, ig, d4, e4);
+    for (; w < wfast_hi; w += nt) {
+      SV_CHECK(4u * w + (uint32_t)__cvta_generic_to_shared(seg) < s_chk_hi, kVioScratch);
+      seg[w] = wheel_word<0, NG>(tabb, ig, d4, e4);
+    }
   }
   for (; w < nwords; w += nt) {
     uint32_t v = wheel_word<0, NG>(tabb, ig, d4, e4);
@@ -198,6 +222,7 @@ __device__ __forceinline__ void wheel_init(uint32_t *seg, const uint32_t *tab, u
     // valid bits i: j0 + 32 i < valid
     const int k = j0 < valid ? (int)((valid - j0 + 31u) >> 5) : 0;
     if (k < 32) v = k <= 0 ? 0xFFFFFFFFu : (v | (0xFFFFFFFFu << k));
+    SV_CHECK(4u * w + (uint32_t)__cvta_generic_to_shared(seg) < s_chk_hi, kVioScratch);
     seg[w] = v;
   }
 }
@@ -590,6 +615,7 @@ __device__ __forceinline__ void bucket_push(const SieveParams &P, uint32_t &cnt,
     if (slot == t) pos = base + __popc(m & ((1u << lane) - 1u));
     if (lane == t) cnt += __popc(m);
   }
+  SV_CHECK(!alive || (pos < P.capw && slot < P.ring), kVioScratch);
   if (alive) bucket_at(P, slot, warp, nw)[pos] = e;
 }
 
@@ -719,6 +745,8 @@ __device__ __forceinline__ void untranspose(uint32_t *seg, uint32_t valid) {
 #pragma unroll
     for (int u = 0; u < kUT; ++u) {
       const uint32_t Bu = B + u * nw;
+      SV_CHECK(Bu >= nblk || 4u * (32u * Bu + lane) + (uint32_t)__cvta_generic_to_shared(seg) < s_chk_hi,
+               kVioScratch);
       if (Bu < nblk) seg[32u * Bu + lane] = kInvert ? ~x[u] : x[u];
     }
   }
@@ -788,6 +816,7 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
     const uint64_t nw = out_words > w0 ? min((uint64_t)4u * nq, out_words - w0) : 0ull;
     n16 = (uint32_t)nw & ~3u;
 #if SIEVE_WB_DIAG != 2
+    SV_CHECK(threadIdx.x != 0 || n16 == 0 || w0 + n16 <= out_words, kVioBitmapStore);
     if (threadIdx.x == 0 && n16) bulk_store(out + w0, seg, 4u * n16);
 #endif
   }
@@ -851,6 +880,7 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
           if (gw + 3 < out_words) out[gw + 3] = x3;
         }
       } else if (vec4 && gw + 4 <= out_words) {
+        SV_CHECK((gw & 3) == 0, kVioBitmapStore);
         reinterpret_cast<uint4 *>(out)[gw >> 2] = make_uint4(x0, x1, x2, x3);
       } else {
         if (gw < out_words) out[gw] = x0;
@@ -967,6 +997,7 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
       // two primes per 16-byte store once the address is 16-byte aligned:
       // the emission is bound by the number of store instructions
       uint64_t *dst = P.list + k;
+      SV_CHECK(k + cx <= P.list_cap, kVioListStore);
       if ((reinterpret_cast<uintptr_t>(dst) & 8u) && x) {
         *dst++ = v0 + 2ull * (uint32_t)(__ffs(x) - 1);
         x &= x - 1;
@@ -977,6 +1008,7 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
         if (x) {
           const uint32_t b2 = __ffs(x) - 1;
           x &= x - 1;
+          SV_CHECK(dst + 2 <= P.list + P.list_cap && ((uintptr_t)dst & 15u) == 0, kVioListStore);
           *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(v0 + 2ull * b1, v0 + 2ull * b2);
           dst += 2;
         } else {
@@ -1217,6 +1249,7 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
   const uint32_t nbits = i0 <= imax ? min(L, imax - i0 + 1u) : 0u;
   const uint32_t nwd = (nbits + 31u) >> 5;
   const uint32_t a = 2u * i0 + 1u;
+  SV_CHECK(4u * nwd + (uint32_t)__cvta_generic_to_shared(bm) <= s_chk_hi, kVioScratch);  // fused_fits
   for (uint32_t w = tid; w < nwd; w += blockDim.x) {
     uint32_t v = pattern_word(i0 + 32u * w);
     if (blockIdx.x == 0 && w == 0) v &= ~kSelfPat;  // 3..31 are prime
@@ -1272,6 +1305,7 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
     while (x) {
       const uint32_t b = __ffs(x) - 1u;
       x &= x - 1u;
+      SV_CHECK(4u * q + (uint32_t)__cvta_generic_to_shared(stage) < s_chk_hi, kVioScratch);
       stage[q++] = a + 2u * (32u * w + b);
     }
     o += row;
@@ -1362,6 +1396,13 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   const uint32_t sb = (sraw + (kSmemAlign - 1u)) & ~(kSmemAlign - 1u);
   uint32_t *seg = smem + (sb - sraw) / 4u;
   uint32_t *tab = seg + P.seg_bits / 32;
+#if SIEVE_CHECK_BOUNDS
+  if (threadIdx.x == 0) {
+    s_chk_lo = sb;
+    s_chk_hi = sb + P.seg_bits / 8u;  // S odd slots = S / 32 words
+  }
+  __syncthreads();
+#endif
   __shared__ unsigned long long red[64];
   __shared__ PrimeRegions sR;
   __shared__ uint32_t s_last;
@@ -1390,16 +1431,23 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
   // contiguous runs (the buckets carry each large prime from one segment of
   // the run to the next)
   const bool buckets = MODE != kBatch && P.buckets != nullptr && !(P.flags & kFlagSkipMarking);
-  const uint64_t s_begin = buckets ? blockIdx.x * P.nseg / gridDim.x : blockIdx.x;
-  const uint64_t s_end = buckets ? (blockIdx.x + 1ull) * P.nseg / gridDim.x : P.nseg;
+  const uint64_t nseg = (MODE == kBatch && P.nitems) ? (uint64_t)__ldg(P.nitems) : P.nseg;
+  const uint64_t s_begin = buckets ? blockIdx.x * nseg / gridDim.x : blockIdx.x;
+  const uint64_t s_end = buckets ? (blockIdx.x + 1ull) * nseg / gridDim.x : nseg;
   const uint64_t s_step = buckets ? 1u : gridDim.x;
   // fused A2: the base primes, then the first segment's wheel pattern while
   // the other CTAs finish theirs (between arrive and wait of the last barrier)
   const bool pre_init = MODE != kBatch && P.bprimes && s_begin < s_end;
+  // diagnostics (kFlagReverse, bitmap mode without buckets): the CTA's
+  // segments in the reverse order -- schedule invariance.  Compiled into the
+  // bitmap kernel only: the count kernel's code generation is sensitive to
+  // its segment loop (a same-box A/B measured +2 % with it there)
+  const bool reverse = MODE == kBitmap && !buckets && (P.flags & kFlagReverse);
   if (MODE != kBatch && P.bprimes) {
     base_phase(P, seg);
     if (pre_init) {
-      const uint64_t bit0 = s_begin * (uint64_t)P.seg_bits, left = P.nbits - bit0;
+      const uint64_t s0 = reverse ? P.nseg - 1u - s_begin : s_begin;
+      const uint64_t bit0 = s0 * (uint64_t)P.seg_bits, left = P.nbits - bit0;
       wheel_init<NG, kWheelUnrollOf>(seg, tab, P.o0, bit0, left < P.seg_bits ? (uint32_t)left : P.seg_bits,
                                      P.o0 + 2ull * bit0);
     }
@@ -1431,14 +1479,15 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     bucket_fill(P, sR, bcnt, s_begin, s_end);
     bq = (uint32_t)(s_begin % P.ring);
   }
-  for (uint64_t s = s_begin; s < s_end; s += s_step) {
+  for (uint64_t s_it = s_begin; s_it < s_end; s_it += s_step) {
+    const uint64_t s = reverse ? P.nseg - 1u - s_it : s_it;
     uint64_t a, bit0, o0;
     uint32_t valid;
     PrimeRegions Ri = sR;
     if (MODE == kBatch) {
       const BatchItem it = P.items[s];
       a = it.a; valid = it.valid; o0 = it.a; bit0 = 0;
-      // the item's primes are the prefix < it.nend (k_item_ends): clamp the
+      // the item's primes are the prefix < it.nend (k_plan_emit): clamp the
       // regions, no search and no barrier per item
       Ri.end = min(Ri.end, it.nend);
       Ri.start = min(Ri.start, Ri.end);
@@ -1456,12 +1505,12 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       a = o0 + 2ull * bit0;
     }
     const long long c0 = P.prof ? clock64() : 0;
-    if (!(pre_init && s == s_begin)) wheel_init<NG, kWheelUnrollOf>(seg, tab, o0, bit0, valid, a);
+    if (!(pre_init && s_it == s_begin)) wheel_init<NG, kWheelUnrollOf>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
     if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);
     if (buckets) {
-      bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s), valid);
+      bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s_it), valid);
       bq = bq + 1u == P.ring ? 0u : bq + 1u;
     }
     __syncthreads();
@@ -1674,13 +1723,110 @@ __global__ void k_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_
     recips[i] = recip_of(primes[i]);
 }
 
-// A10: the prime prefix of every batch item (first index with p > r_item)
-__global__ void k_item_ends(BatchItem *items, uint64_t n, const uint32_t *__restrict__ primes,
-                            const uint32_t *__restrict__ nbase) {
+// ---------------------------------------------------------------------------
+// A10 planning on the device (internal.h launch_batch_plan).  Three small
+// kernels, no host round trip: per-interval item counts and cost classes
+// (with the histogram of items per class), one CTA scanning the classes
+// largest first, per-interval emission of its items at its class cursor.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t isqrt_dev(uint64_t x) {  // x < 2^53
+  uint64_t r = (uint64_t)sqrt((double)x);
+  while (r * r > x) --r;
+  while ((r + 1) * (r + 1) <= x) ++r;
+  return r;
+}
+
+struct PlanIv {  // one interval's plan
+  uint64_t B;     // odd slots
+  uint32_t k;     // items (0: empty or over kcap)
+  uint32_t cls;   // cost class (larger = costlier)
+  uint32_t r;     // isqrt(hi - 1)
+  bool two, over;
+};
+
+__device__ __forceinline__ PlanIv plan_interval(uint64_t lo, uint64_t hi, uint32_t S,
+                                                uint64_t width_max) {
+  PlanIv v;
+  v.B = hi > lo ? hi / 2 - lo / 2 : 0;
+  const uint64_t k = (v.B + S - 1) / S;  // <= the runtime's kcap when hi - lo <= width_max
+  v.over = hi - lo > width_max;
+  v.k = v.over ? 0u : (uint32_t)k;
+  v.r = hi >= 2 ? (uint32_t)isqrt_dev(hi - 1) : 0u;
+  v.two = lo <= 2 && 2 < hi;
+  // cost of one item: its slots plus one first-hit reduction per base prime
+  const float np = v.r > 2 ? (float)v.r / __logf((float)v.r) : 1.0f;
+  const float cost = 0.6f * (float)(v.k ? v.B / v.k : 0) + 20.0f * np;
+  v.cls = (uint32_t)min(kPlanBuckets - 1.0f, fmaxf(0.0f, 8.0f * __log2f(fmaxf(cost, 1.0f))));
+  return v;
+}
+
+__global__ void k_plan_count(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint32_t S,
+                             uint64_t width_max, uint32_t *hist, uint64_t *result) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const PlanIv v = plan_interval(lo[i], hi[i], S, width_max);
+    if (v.k) atomicAdd(hist + v.cls, v.k);
+    result[2 * i] = v.over ? ~0ull : (v.two ? 1ull : 0ull);
+    result[2 * i + 1] = v.over ? ~0ull : (v.two ? 2ull : 0ull);
+  }
+}
+
+// one CTA of kPlanBuckets threads: cursor[c] = items of the classes above c
+__global__ void k_plan_scan(uint32_t *hist, uint32_t *cursor, uint32_t *nitems) {
+  __shared__ uint32_t sh[kPlanBuckets];
+  const uint32_t t = threadIdx.x;
+  const uint32_t c = kPlanBuckets - 1u - t;  // descending cost
+  sh[t] = hist[c];
+  __syncthreads();
+  for (uint32_t d = 1; d < kPlanBuckets; d <<= 1) {  // inclusive Hillis-Steele scan
+    const uint32_t y = t >= d ? sh[t - d] : 0u;
+    __syncthreads();
+    sh[t] += y;
+    __syncthreads();
+  }
+  cursor[c] = sh[t] - hist[c];
+  if (t == kPlanBuckets - 1u) *nitems = sh[t];
+  __syncthreads();
+  hist[c] = 0u;  // ready for the next plan
+}
+
+__global__ void k_plan_emit(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint32_t S,
+                            uint64_t width_max, uint32_t *cursor, const uint32_t *__restrict__ primes,
+                            const uint32_t *__restrict__ nbase, BatchItem *items) {
   const uint32_t nb = *nbase;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    items[i].nend = upper_bound_u32(primes, nb, items[i].r);
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t l = lo[i];
+    const PlanIv v = plan_interval(l, hi[i], S, width_max);
+    if (!v.k) continue;
+    const uint32_t pos = atomicAdd(cursor + v.cls, v.k);
+    const uint32_t nend = upper_bound_u32(primes, nb, v.r);
+    const uint64_t q = v.B / v.k, rem = v.B % v.k;
+    uint64_t b = 0;
+    for (uint32_t t = 0; t < v.k; ++t) {
+      BatchItem it;
+      it.a = (l | 1u) + 2 * b;
+      it.valid = (uint32_t)(q + (t < rem ? 1 : 0));
+      it.interval = (uint32_t)i;
+      it.r = v.r;
+      it.nend = nend;
+      b += it.valid;
+      items[pos + t] = it;
+    }
+  }
+}
+
+cudaError_t launch_batch_plan(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint32_t S,
+                              uint64_t width_max, const uint32_t *primes, const uint32_t *nbase,
+                              uint32_t *scratch, BatchItem *items, uint32_t *nitems,
+                              uint64_t *result, cudaStream_t s) {
+  uint32_t *hist = scratch, *cursor = scratch + kPlanBuckets;
+  const uint64_t blocks = (n + 255) / 256;
+  const int g = (int)(blocks < 1184 ? (blocks ? blocks : 1) : 1184);
+  k_plan_count<<<g, 256, 0, s>>>(lo, hi, n, S, width_max, hist, result);
+  k_plan_scan<<<1, kPlanBuckets, 0, s>>>(hist, cursor, nitems);
+  k_plan_emit<<<g, 256, 0, s>>>(lo, hi, n, S, width_max, cursor, primes, nbase, items);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -1763,6 +1909,15 @@ int sieve_max_ctas_per_sm(int ng, int mode, int threads, size_t smem) {
   return occ_t<4, kCount>(threads, smem);
 }
 
+cudaError_t read_violations(unsigned long long *out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_violations, sizeof(unsigned long long) * kVioClasses);
+  if (e == cudaSuccess && reset) {
+    static const unsigned long long zero[kVioClasses] = {};
+    e = cudaMemcpyToSymbol(g_violations, zero, sizeof zero);
+  }
+  return e;
+}
+
 uint32_t base_slices(uint32_t r) {
   const uint32_t imax = r >= 3 ? (r - 1) / 2 : 0;
   return (imax + kSliceBits - 1) / kSliceBits;
@@ -1785,11 +1940,5 @@ cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64
   return cudaGetLastError();
 }
 
-cudaError_t launch_item_ends(BatchItem *items, uint64_t n, const uint32_t *primes,
-                             const uint32_t *nbase, cudaStream_t s) {
-  const uint64_t blocks = (n + 255) / 256;
-  k_item_ends<<<(int)(blocks < 1184 ? (blocks ? blocks : 1) : 1184), 256, 0, s>>>(items, n, primes, nbase);
-  return cudaGetLastError();
-}
 
 }  // namespace sv

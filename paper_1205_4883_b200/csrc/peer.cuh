@@ -19,7 +19,10 @@
 // same parity only after finishing e + 1, which needed every rank's e + 1
 // publication, which each rank makes only after it has read all of e.
 // A wait longer than timeout_ns (a peer that never launched) ends with the
-// sentinel result (2^64-1, 2^64-1) instead of a hung GPU.
+// sentinel result (2^64-1, 2^64-1) instead of a hung GPU.  peer_publish alone
+// (sieve_peer_publish_async) makes a rank's share visible without waiting,
+// so that no two kernels ever wait on each other (the cross-process test on
+// one GPU).
 #pragma once
 #include <cstdint>
 
@@ -50,13 +53,10 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-// One thread.  (c, s): this rank's result; returns the sums over all ranks
-// (mod 2^64), or (2^64-1, 2^64-1) on timeout.
-static __device__ __forceinline__ ulonglong2 peer_allreduce(unsigned long long *const *peers,
-                                                         uint32_t world, uint32_t rank,
-                                                         uint64_t epoch, uint64_t timeout_ns,
-                                                         unsigned long long c,
-                                                         unsigned long long s) {
+// One thread: this rank's (c, s) into slot [epoch & 1][rank] of every slab.
+static __device__ __forceinline__ void peer_publish(unsigned long long *const *peers, uint32_t world,
+                                                    uint32_t rank, uint64_t epoch,
+                                                    unsigned long long c, unsigned long long s) {
   const uint32_t base = (uint32_t)(epoch & 1u) * kMaxPeers;
   for (uint32_t q = 0; q < world; ++q) {
     unsigned long long *slot = peers[q] + 4 * (base + rank);
@@ -64,6 +64,17 @@ static __device__ __forceinline__ ulonglong2 peer_allreduce(unsigned long long *
     st_relaxed_sys(slot + 1, s);
     st_release_sys(slot + 2, epoch);
   }
+}
+
+// One thread.  (c, s): this rank's result; returns the sums over all ranks
+// (mod 2^64), or (2^64-1, 2^64-1) on timeout.
+static __device__ __forceinline__ ulonglong2 peer_allreduce(unsigned long long *const *peers,
+                                                         uint32_t world, uint32_t rank,
+                                                         uint64_t epoch, uint64_t timeout_ns,
+                                                         unsigned long long c,
+                                                         unsigned long long s) {
+  peer_publish(peers, world, rank, epoch, c, s);
+  const uint32_t base = (uint32_t)(epoch & 1u) * kMaxPeers;
   const unsigned long long *mine = peers[rank];
   const unsigned long long t0 = global_ns();
   ulonglong2 tot = make_ulonglong2(0, 0);

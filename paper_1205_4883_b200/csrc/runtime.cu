@@ -3,10 +3,15 @@
 // Responsibilities: argument validation (error codes of sieve.h), planning of
 // a call (step A1: odd-only grid, segments, grid size), device scratch owned
 // by the library, stream handling, host<->device staging for host outputs,
-// and the launch sequences of the three north_star calls:
-//   count  : K1 base primes -> sieve(count) [last CTA reduces]     2 launches
-//   bitmap : K1 -> sieve(bitmap, 128-bit write-back)                2 launches
-//   primes : K1 -> sieve(bitmap->scratch, seg counts) -> scan -> compact
+// and the launch sequences of the three north_star calls.  Each is ONE sieve
+// launch: the base primes (A2) are computed inside it (fused A2, a
+// cooperative launch with two grid barriers), then
+//   count  : A3-A6, the last CTA reduces the per-CTA (count, sum)
+//   bitmap : A3-A7, one TMA bulk copy of each segment's words to HBM
+//   primes : A3, A4/A5, A8 per-segment decoupled look-back + compaction
+// When the cooperative launch is not possible (a slice of the odd numbers
+// <= r does not fit a segment, or the launch is refused) the base-prime
+// kernel K1 runs first and the sieve is an ordinary launch.
 // No C++ exception crosses the ABI; there is no CPU fallback.
 #include <cuda_runtime.h>
 
@@ -29,6 +34,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_coop_fallbacks{0};  // refused cooperative launches (diagnostics)
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -126,6 +132,9 @@ struct Ctx {
   DevBuf<uint64_t> list;
   DevBuf<sv::BatchItem> items;
   DevBuf<uint64_t> bres;
+  DevBuf<uint64_t> blo, bhi;        // batch: the intervals, on the device
+  DevBuf<uint32_t> plan;            // batch: class histogram + cursors (hist kept zero)
+  DevBuf<uint32_t> nitems;          // batch: the planned item count
   DevBuf<uint2> buckets;  // step A5 bucket rings
   DevBuf<uint64_t> kflags;  // K1 look-back flags (epoch-tagged, never reset)
   uint32_t epoch = 0;
@@ -231,17 +240,25 @@ int ensure_smem_attr() {
   return 0;
 }
 
+// resident sieve CTAs per SM for the current (threads, shared memory), from
+// the occupancy query, cached per key and refreshed whenever the key changes
+int occupancy() {
+  const size_t key = sieve_smem() * 2048 + g.opt.threads;
+  if (g.occ_key != key) {
+    g.occ = sv::sieve_max_ctas_per_sm(0, 0, (int)g.opt.threads, sieve_smem());
+    g.occ_key = key;
+  }
+  return g.occ > 0 ? g.occ : 1;
+}
+
+// Persistent grid: nsm x (resident CTAs per SM).  An explicit ctas_per_sm is
+// clamped to the occupancy: every CTA of a launch must be resident (the
+// fused A2's grid barriers and the list mode's look-back wait on CTAs of the
+// same launch).
 int grid_for(uint64_t nseg) {
   if (g.nsm <= 0) return 148;  // before the device is initialised (planning only)
-  int per = g.opt.ctas_per_sm;
-  if (per <= 0) {  // occupancy query cached per (threads, shared-memory size)
-    const size_t key = sieve_smem() * 2048 + g.opt.threads;
-    if (g.occ_key != key) {
-      g.occ = sv::sieve_max_ctas_per_sm(0, 0, (int)g.opt.threads, sieve_smem());
-      g.occ_key = key;
-    }
-    per = g.occ > 0 ? g.occ : 1;
-  }
+  const int occ = occupancy();
+  int per = g.opt.ctas_per_sm > 0 ? std::min((int)g.opt.ctas_per_sm, occ) : occ;
   uint64_t grid = (uint64_t)g.nsm * per;
   if (grid > nseg) grid = nseg;
   return grid < 1 ? 1 : (int)grid;
@@ -391,7 +408,8 @@ struct BaseReq {
 // primes staged for emission (<= L/3 + 2: one of three consecutive odd
 // numbers is a multiple of 3)
 bool fused_fits(uint64_t r, int grid, uint64_t sbits) {
-  if (g.opt.ctas_per_sm > 0 && (int)g.opt.ctas_per_sm > g.occ) return false;  // not co-resident
+  if (g.flags & sv::kFlagNoCoop) return false;       // diagnostics: the K1 + ordinary-launch path
+  if (grid > g.nsm * occupancy()) return false;      // not co-resident (grid_for clamps: never)
   const uint64_t imax = r >= 3 ? (r - 1) / 2 : 0;
   const uint64_t L = ((imax + grid - 1) / grid + 31) / 32 * 32;
   return sv::kMaxSmallWords + 128 + L / 32 + L / 3 + 2 <= sbits / 32;
@@ -400,32 +418,42 @@ bool fused_fits(uint64_t r, int grid, uint64_t sbits) {
 int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork, const BaseReq *req = nullptr) {
   TRY(ensure_smem_attr());
   const int grid = grid_for(nwork);
+  sp.partials = g.partials.p;  // [2], zeroed at init, reset by every launch's last CTA
+  // not in list mode: its look-back needs the segments of a wave in flight
+  // together (round robin), a CTA's contiguous run would serialise it
+  if (mode == sv::kCount || mode == sv::kBitmap) TRY(setup_buckets(sp, grid));
+  const int ng = ng_for_wheel(g.opt.wheel);
   if (req) {
+    sp.primes = req->primes;
+    sp.recips = req->recips;
+    sp.nbase = req->nbase;
     if (fused_fits(req->r, grid, sp.seg_bits)) {
       if (!g.gbar.p) {
         TRY(g.gbar.ensure(1));
         CUDA_TRY(cudaMemsetAsync(g.gbar.p, 0, sizeof(unsigned int), g.stream()));
       }
       TRY(g.bcounts.ensure((size_t)grid + 7));  // counts, then the region boundaries
-      sp.bprimes = req->primes;
-      sp.brecips = req->recips;
-      sp.bnbase = req->nbase;
-      sp.bcap = (uint32_t)std::min<uint64_t>(req->cap, 0xFFFFFFFFull);
-      sp.rs = (uint32_t)isqrt_u64(req->r);
-      sp.bcounts = g.bcounts.p;
-      sp.gbar = g.gbar.p;
-    } else {
-      TRY(base_primes(req->r, req->primes, req->recips, req->cap, req->nbase, g.stream()));
+      sv::SieveParams fp = sp;
+      fp.bprimes = req->primes;
+      fp.brecips = req->recips;
+      fp.bnbase = req->nbase;
+      fp.bcap = (uint32_t)std::min<uint64_t>(req->cap, 0xFFFFFFFFull);
+      fp.rs = (uint32_t)isqrt_u64(req->r);
+      fp.bcounts = g.bcounts.p;
+      fp.gbar = g.gbar.p;
+      const cudaError_t e = sv::launch_sieve(ng, mode, fp, grid, (int)g.opt.threads, sieve_smem(), g.stream());
+      if (e == cudaSuccess) {
+        g_launches += 1;
+        return 0;
+      }
+      // the cooperative launch was refused (e.g. not every CTA can be
+      // resident under MPS or a co-tenant): nothing ran; clear the
+      // (non-sticky) launch error and take the K1 + ordinary-launch path
+      cudaGetLastError();
+      g_coop_fallbacks += 1;
     }
-    sp.primes = req->primes;
-    sp.recips = req->recips;
-    sp.nbase = req->nbase;
+    TRY(base_primes(req->r, req->primes, req->recips, req->cap, req->nbase, g.stream()));
   }
-  sp.partials = g.partials.p;  // [2], zeroed at init, reset by every launch's last CTA
-  // not in list mode: its look-back needs the segments of a wave in flight
-  // together (round robin), a CTA's contiguous run would serialise it
-  if (mode == sv::kCount || mode == sv::kBitmap) TRY(setup_buckets(sp, grid));
-  const int ng = ng_for_wheel(g.opt.wheel);
   CUDA_TRY(sv::launch_sieve(ng, mode, sp, grid, (int)g.opt.threads, sieve_smem(), g.stream()));
   g_launches += 1;
   return 0;
@@ -446,7 +474,7 @@ int stats_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, c
 }
 
 int bitmap_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase,
-                 uint32_t *out, uint64_t *result, const BaseReq *req = nullptr) {
+                 uint32_t *out, uint64_t *result, const BaseReq *req) {
   if (P.nbits == 0) return stats_async(P, primes, recips, nbase, result, req);
   sv::SieveParams sp = params_for(P, primes, recips, nbase, result);
   sp.out = out;
@@ -621,72 +649,62 @@ int64_t do_primes(uint64_t lo, uint64_t hi, uint64_t *out, uint64_t cap) {
   return (int64_t)c;
 }
 
+// Step A10 on device-resident intervals: base primes <= isqrt(hi_max - 1)
+// (K1), the plan on the device (launch_batch_plan: items of <= S odd slots,
+// largest cost class first), then the batch sieve over the planned items.
+// result: [2 n] (count, sum mod 2^64) per interval, overwritten.
+int batch_async(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t hi_max,
+                uint64_t width_max, uint64_t *result) {
+  if (n == 0) return 0;
+  if (n > 0xFFFFFFFFull) return fail(SIEVE_EINVAL, "n = %llu intervals > 2^32 - 1", (unsigned long long)n);
+  if (hi_max > SIEVE_MAX_HI) return fail(SIEVE_ERANGE, "hi_max > 2^48");
+  const uint64_t S = seg_bits();
+  const uint64_t kcap = (width_max / 2 + 1 + S - 1) / S + 1;  // items of one interval, at most
+  if (n * kcap > 0xFFFFFFFFull) return fail(SIEVE_EINVAL, "too many batch items");
+  const uint64_t rmax = hi_max >= 2 ? isqrt_u64(hi_max - 1) : 0;
+  TRY(own_base(rmax));
+  if (!g.plan.p) {
+    TRY(g.plan.ensure(2 * sv::kPlanBuckets));
+    CUDA_TRY(cudaMemsetAsync(g.plan.p, 0, 2 * sv::kPlanBuckets * sizeof(uint32_t), g.stream()));
+  }
+  TRY(g.nitems.ensure(1));
+  TRY(g.items.ensure(n * kcap));
+  CUDA_TRY(sv::launch_batch_plan(lo, hi, n, (uint32_t)S, width_max, g.primes.p, g.nbase.p,
+                                 g.plan.p, g.items.p, g.nitems.p, result, g.stream()));
+  g_launches += 3;
+  Plan dummy = make_plan(0, 0);
+  sv::SieveParams sp = params_for(dummy, g.primes.p, g.recips.p, g.nbase.p, result);
+  sp.items = g.items.p;
+  sp.nitems = g.nitems.p;
+  sp.nseg = n * kcap;  // bound for the grid size; the kernel reads *nitems
+  sp.r = (uint32_t)rmax;
+  return run_sieve(sv::kBatch, sp, n * kcap);
+}
+
 int do_batch(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t *count, uint64_t *sum) {
   if (n == 0) return 0;
   if (!lo || !hi || !count || !sum) return fail(SIEVE_EINVAL, "NULL array in sieve_batch");
-  uint64_t maxhi = 0;
+  uint64_t hi_max = 0, width_max = 0;
   for (uint64_t i = 0; i < n; ++i) {
     TRY(validate(lo[i], hi[i]));
-    maxhi = std::max(maxhi, hi[i]);
+    hi_max = std::max(hi_max, hi[i]);
+    width_max = std::max(width_max, hi[i] - lo[i]);
   }
   TRY(ensure_ready());
-  // step A10 plan: an interval of B odd slots becomes ceil(B / S) items of
-  // equal size (one segment each), and the items are dealt largest first
-  // (their cost: the slots plus one first-hit reduction per base prime <= r)
-  const uint64_t S = seg_bits();
-  std::vector<sv::BatchItem> items;
-  std::vector<double> cost;
-  for (uint64_t i = 0; i < n; ++i) {
-    const Plan P = make_plan(lo[i], hi[i]);
-    if (P.nbits == 0) continue;
-    const uint64_t k = (P.nbits + S - 1) / S, q = P.nbits / k, rem = P.nbits % k;
-    const double np = P.r > 2 ? (double)P.r / std::log((double)P.r) : 1.0;
-    uint64_t b = 0;
-    for (uint64_t t = 0; t < k; ++t) {
-      sv::BatchItem it;
-      it.a = P.o0 + 2 * b;
-      it.valid = (uint32_t)(q + (t < rem ? 1 : 0));
-      it.interval = (uint32_t)i;
-      it.r = (uint32_t)P.r;
-      it.nend = 0;
-      b += it.valid;
-      items.push_back(it);
-      cost.push_back(0.6 * it.valid + 20.0 * np);
-    }
-  }
-  {
-    std::vector<uint32_t> ord(items.size());
-    for (uint32_t t = 0; t < ord.size(); ++t) ord[t] = t;
-    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) { return cost[x] > cost[y]; });
-    std::vector<sv::BatchItem> sorted(items.size());
-    for (uint32_t t = 0; t < ord.size(); ++t) sorted[t] = items[ord[t]];
-    items.swap(sorted);
-  }
-  const uint64_t rmax = maxhi >= 2 ? isqrt_u64(maxhi - 1) : 0;
-  TRY(own_base(rmax));
+  // the intervals to the device, the plan and the sieve there, the results back
+  TRY(g.blo.ensure(n));
+  TRY(g.bhi.ensure(n));
   TRY(g.bres.ensure(2 * n));
-  CUDA_TRY(cudaMemsetAsync(g.bres.p, 0, 2 * n * sizeof(uint64_t), g.stream()));
-  if (!items.empty()) {
-    TRY(g.items.ensure(items.size()));
-    CUDA_TRY(cudaMemcpyAsync(g.items.p, items.data(), items.size() * sizeof(sv::BatchItem),
-                             cudaMemcpyHostToDevice, g.stream()));
-    CUDA_TRY(sv::launch_item_ends(g.items.p, items.size(), g.primes.p, g.nbase.p, g.stream()));
-    g_launches += 1;
-    Plan dummy = make_plan(0, 0);
-    sv::SieveParams sp = params_for(dummy, g.primes.p, g.recips.p, g.nbase.p, g.bres.p);
-    sp.items = g.items.p;
-    sp.nseg = items.size();
-    sp.r = (uint32_t)rmax;
-    TRY(run_sieve(sv::kBatch, sp, items.size()));
-  }
+  CUDA_TRY(cudaMemcpyAsync(g.blo.p, lo, n * 8, cudaMemcpyHostToDevice, g.stream()));
+  CUDA_TRY(cudaMemcpyAsync(g.bhi.p, hi, n * 8, cudaMemcpyHostToDevice, g.stream()));
+  TRY(batch_async(g.blo.p, g.bhi.p, n, hi_max, width_max, g.bres.p));
   std::vector<uint64_t> h(2 * n);
   CUDA_TRY(cudaMemcpyAsync(h.data(), g.bres.p, 2 * n * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                            g.stream()));
   CUDA_TRY(cudaStreamSynchronize(g.stream()));
   for (uint64_t i = 0; i < n; ++i) {
-    const bool two = lo[i] <= 2 && 2 < hi[i];
-    count[i] = h[2 * i] + (two ? 1 : 0);
-    sum[i] = h[2 * i + 1] + (two ? 2 : 0);
+    count[i] = h[2 * i];
+    sum[i] = h[2 * i + 1];
   }
   return 0;
 }
@@ -792,6 +810,15 @@ int sieve_batch(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t *co
   return do_batch(lo, hi, n, count, sum_mod_2_64);
 }
 
+int sieve_batch_async(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t hi_max,
+                      uint64_t width_max, uint64_t *result) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (n == 0) return 0;
+  if (!lo || !hi || !result) return fail(SIEVE_EINVAL, "NULL array in sieve_batch_async");
+  TRY(ensure_ready());
+  return batch_async(lo, hi, n, hi_max, width_max, result);
+}
+
 uint64_t sieve_base_capacity(uint64_t r) { return base_capacity(r); }
 
 int sieve_base_primes_async(uint64_t r, uint32_t *primes, uint64_t *recips, uint64_t cap,
@@ -846,7 +873,21 @@ int sieve_bitmap_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const u
   const Plan P = make_plan(lo, hi);
   if (P.words && !out) return fail(SIEVE_EINVAL, "NULL out");
   TRY(ensure_ready());
-  return bitmap_async(P, primes, recips, nbase, out, result);
+  return bitmap_async(P, primes, recips, nbase, out, result, nullptr);
+}
+
+int sieve_bitmap_base_async(uint64_t lo, uint64_t hi, uint32_t *primes, uint64_t *recips,
+                            uint32_t *nbase, uint64_t cap, uint32_t *out, uint64_t *result) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  TRY(validate(lo, hi));
+  if (!primes || !recips || !nbase || !result) return fail(SIEVE_EINVAL, "NULL buffer");
+  const Plan P = make_plan(lo, hi);
+  if (P.words && !out) return fail(SIEVE_EINVAL, "NULL out");
+  if (cap < base_capacity(P.r)) return fail(SIEVE_EINVAL, "cap %llu < sieve_base_capacity(%llu)",
+                                            (unsigned long long)cap, (unsigned long long)P.r);
+  TRY(ensure_ready());
+  const BaseReq q{primes, recips, nbase, cap, P.r};
+  return bitmap_async(P, primes, recips, nbase, out, result, &q);
 }
 
 int sieve_peer_slab_handle(void *handle_out) {
@@ -930,6 +971,19 @@ int sieve_stats_allreduce_async(uint64_t lo, uint64_t hi, const uint32_t *primes
   return stats_allreduce_async(make_plan(lo, hi), primes, recips, nbase, result);
 }
 
+int sieve_peer_publish_async(uint64_t count, uint64_t sum) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (g.peer.world == 0) return fail(SIEVE_EINVAL, "no peers attached (sieve_peer_attach)");
+  TRY(ensure_ready());
+  auto &pe = g.peer;
+  pe.epoch += 1;
+  TRY(g.result.ensure(2));
+  CUDA_TRY(sv::launch_peer_only(pe.ptrs.p, pe.world, pe.rank, pe.epoch, pe.timeout_ns, count, sum,
+                                g.result.p, g.stream(), /*wait=*/false));
+  g_launches += 1;
+  return 0;
+}
+
 int sieve_set_device(int ordinal) {
   std::lock_guard<std::mutex> lk(g.mu);
   int ndev = 0;
@@ -945,6 +999,18 @@ int sieve_set_device(int ordinal) {
 
 int sieve_set_stream(void *cuda_stream) {
   std::lock_guard<std::mutex> lk(g.mu);
+  const cudaStream_t next = cuda_stream ? (cudaStream_t)cuda_stream : g.own;
+  if (g.ready && next != g.stream()) {
+    // every launch shares the library's scratch (partials, tickets, grid
+    // barrier, look-back flags, result): work on the new stream starts only
+    // after the work already queued on the old one
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaError_t e = cudaEventRecord(ev, g.stream());
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(next, ev, 0);
+    cudaEventDestroy(ev);
+    CUDA_TRY(e);
+  }
   g.user = (cudaStream_t)cuda_stream;
   g.user_set = cuda_stream != nullptr;
   return 0;
@@ -1008,6 +1074,7 @@ void sieve_shutdown(void) {
   g.tables.release(); g.primes.release(); g.recips.release(); g.nbase.release();
   g.partials.release(); g.done.release(); g.result.release(); g.bitmap.release();
   g.list.release(); g.items.release(); g.bres.release();
+  g.blo.release(); g.bhi.release(); g.plan.release(); g.nitems.release();
   g.buckets.release(); g.kflags.release(); g.lflags.release(); g_f2.buf.release();
   g.gbar.release(); g.bcounts.release();  // fused A2 (re-created, zeroed, on demand)
   peer_detach();
@@ -1063,11 +1130,35 @@ int sieve_is_prime(const uint64_t *nums, uint64_t n, uint8_t *out) {
 
 int sieve_debug_set_flags(uint32_t flags) {
   std::lock_guard<std::mutex> lk(g.mu);
-  if (flags & ~(sv::kFlagSkipMarking | sv::kFlagSkipA | sv::kFlagSkipB | sv::kFlagSkipC))
+  if (flags & ~(sv::kFlagSkipMarking | sv::kFlagSkipA | sv::kFlagSkipB | sv::kFlagSkipC |
+                sv::kFlagReverse | sv::kFlagNoCoop))
     return fail(SIEVE_EINVAL, "unknown debug flags %u", flags);
   g.flags = flags;
   return 0;
 }
+
+int sieve_debug_violations(uint64_t *out, int reset) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!out) return fail(SIEVE_EINVAL, "NULL out");
+  TRY(ensure_ready());
+  CUDA_TRY(cudaStreamSynchronize(g.stream()));
+  unsigned long long v[sv::kVioClasses];
+  CUDA_TRY(sv::read_violations(v, reset != 0));
+  for (int k = 0; k < sv::kVioClasses; ++k) out[k] = v[k];
+  return SIEVE_CHECK_BOUNDS;
+}
+
+int sieve_debug_k0(double *lanes_per_clk_per_sm, double *sm_ghz) {
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!lanes_per_clk_per_sm || !sm_ghz) return fail(SIEVE_EINVAL, "NULL output");
+  TRY(ensure_ready());
+  CUDA_TRY(cudaStreamSynchronize(g.stream()));
+  CUDA_TRY(sv::k0_smem_atomic_rate(g.nsm, lanes_per_clk_per_sm, sm_ghz));
+  g_launches += 3;
+  return 0;
+}
+
+uint64_t sieve_debug_coop_fallbacks(void) { return g_coop_fallbacks.load(); }
 
 int sieve_debug_set_profile(uint64_t *dev_counters) {
   std::lock_guard<std::mutex> lk(g.mu);

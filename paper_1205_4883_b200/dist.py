@@ -134,8 +134,10 @@ def attach_peers(group=None, timeout_ms: int = 10000, backend=None) -> bool:
     before anyone's first fused launch.  Later stats(..., fused=True) calls
     on this group all-reduce inside the sieve kernel.  Every rank takes part
     in every collective even when its own export or attach fails, so a local
-    failure cannot leave the others waiting; returns whether THIS rank is
-    attached (callers agree across ranks before using it)."""
+    failure cannot leave the others waiting, and the ranks then agree: the
+    per-rank outcomes are combined with a MIN all-reduce, and if any rank
+    failed every rank detaches -- so the default of stats(fused=None) is the
+    same on every rank (all fused or all NCCL).  Returns the agreed outcome."""
     import torch.distributed as dist
     be = backend if backend is not None else CudaBackend()
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -159,9 +161,28 @@ def attach_peers(group=None, timeout_ms: int = 10000, backend=None) -> bool:
         ok = False
     if world > 1:
         dist.barrier(group=group)
+        ok = _agree_all(ok, group)
     if ok:
         _ATTACHED[id(group)] = world
+    else:
+        try:
+            be.peer_detach()
+        except Exception:  # noqa: BLE001 -- nothing attached on this rank
+            pass
     return ok
+
+
+def _agree_all(ok: bool, group=None) -> bool:
+    """True iff every rank of `group` passed ok=True (MIN all-reduce over the
+    group's backend: a CPU tensor for gloo, a CUDA tensor for NCCL)."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cpu")
+    if dist.get_backend(group) == "nccl":
+        dev = torch.device("cuda", torch.cuda.current_device())
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(t.item())
 
 
 def u64_to_i64(x: int) -> int:
@@ -338,6 +359,16 @@ def bitmap_checksum(words: np.ndarray, first_word: int = 0) -> int:
     return int(np.sum(idx * w, dtype=np.uint64))
 
 
+def bitmap_checksum_tensor(words, first_word: int = 0) -> int:
+    """bitmap_checksum on the tensor's own device (no host copy of the
+    bitmap): int64 products and sums wrap mod 2^64 like u64 arithmetic; the
+    uint32 words are zero-extended from their int32 view."""
+    import torch
+    w = words.to(torch.int64) & 0xFFFFFFFF
+    idx = torch.arange(first_word + 1, first_word + 1 + w.numel(), dtype=torch.int64, device=w.device)
+    return i64_to_u64(int((idx * w).sum().item()))
+
+
 class CudaGatherBackend:
     """The product compute path for F1: per-rank bitmap / list of a block on
     the current device (C ABI), returned as CUDA tensors."""
@@ -353,14 +384,32 @@ class CudaGatherBackend:
         return out[:n]
 
     def primes(self, a, b, device):
+        """ONE list-mode sieve of [a, b): the output is sized by an upper
+        bound on the count instead of a count pass, then trimmed."""
         import torch
         import paper_1205_4883_b200 as sv
-        n = sv.count(a, b)
-        out = torch.zeros(max(n, 1), dtype=torch.int64, device=device)
-        if n:
+        cap = prime_count_bound(a, b)
+        out = torch.zeros(max(cap, 1), dtype=torch.int64, device=device)
+        n = 0
+        if cap:
             with _LibraryStreamOrder():
-                sv.primes(a, b, cap=n, out=out)
+                _, n = sv.primes(a, b, cap=cap, out=out)
+        if n > cap:  # cannot happen (the bound holds for every interval)
+            raise RuntimeError(f"prime_count_bound({a}, {b}) = {cap} < {n}")
         return out[:n]
+
+
+def prime_count_bound(a: int, b: int) -> int:
+    """An upper bound on the number of primes in [a, b), for sizing a list
+    output without a count pass.  Candidates are 2 and 3 plus the integers
+    coprime to 6, at most (b - a) / 3 + 2 of them; for long intervals the
+    Brun-Titchmarsh inequality pi(x + y) - pi(x) <= 2 y / ln y (Montgomery
+    and Vaughan, y > 1) is much tighter.  The smaller of the two, plus 2."""
+    y = max(b - a, 0)
+    cand = y // 3 + 2
+    if y > 1:
+        cand = min(cand, int(2 * y / math.log(y)) + 2)
+    return cand
 
 
 def _gather_padded(t, group, world):
@@ -394,7 +443,7 @@ def gather_bitmap(lo: int, hi: int, group=None, backend=None, device=None):
     a, b = block_of(lo, hi, rank, world)
     mine = be.bitmap(a, b, dev)
     w0 = _block_words(lo, hi, world)[rank][0]
-    part = bitmap_checksum(mine.cpu().numpy().view(np.uint32), w0)
+    part = bitmap_checksum_tensor(mine, w0)
     cs = torch.tensor([u64_to_i64(part)], dtype=torch.int64, device=dev)
     if world > 1:
         dist.all_reduce(cs, op=dist.ReduceOp.SUM, group=group)

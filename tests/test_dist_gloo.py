@@ -172,7 +172,9 @@ def _worker(rank, world, port, q, tmpdir=None):
         ok = D.attach_peers(backend=fb)
         t = torch.tensor([1 if ok else 0], dtype=torch.int32)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        out["attach_ok"] = (bool(ok), bool(t.item()))
+        # attach_peers itself agrees: every rank reports the failure and the
+        # default of stats(fused=None) is NCCL/gloo everywhere
+        out["attach_ok"] = (bool(ok), bool(t.item()), id(None) in D._ATTACHED, fb.views is None)
         D.detach_peers(backend=fb)
         out["after_fail"] = D.stats(2, 10**5 + 1, backend=be, device=cpu)
         q.put((rank, out))
@@ -192,7 +194,8 @@ def test_two_rank_gloo_stats_batch_and_wrap():
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert res[0]["attach_ok"] == (True, False) and res[1]["attach_ok"] == (False, False)
+    assert res[0]["attach_ok"] == (False, False, False, True)
+    assert res[1]["attach_ok"] == (False, False, False, True)
     assert res[0]["after_fail"] == res[1]["after_fail"] == oracle.stats(2, 10**5 + 1)
     for rr in res.values():
         del rr["attach_ok"]
@@ -259,3 +262,20 @@ def test_lpt_assignment_properties():
         loads = np.array([cost[p].sum() for p in parts])
         # LPT is within 4/3 of optimal; here the spread is tiny
         assert loads.max() <= loads.mean() * 1.05 + cost.max()
+
+
+def test_prime_count_bound_and_device_checksum():
+    """F1 helpers: the list-capacity bound holds (it sizes gather_primes'
+    single list-mode pass), and the on-device decomposable checksum equals
+    the host one, wrap-around included."""
+    for lo, hi in [(0, 0), (0, 3), (2, 3), (0, 100), (2, 10**6), (10**12, 10**12 + 10**6),
+                   (10**9, 10**9 + 7), (999_999_999_989, 1_000_000_000_039)]:
+        assert D.prime_count_bound(lo, hi) >= oracle.stats(lo, hi)[0], (lo, hi)
+    for x in (10**7, 10**8, 10**9):  # pi(x) from known_pi.txt
+        pi = {10**7: 664579, 10**8: 5761455, 10**9: 50847534}[x]
+        assert D.prime_count_bound(0, x + 1) >= pi
+    rng = np.random.default_rng(5)
+    w = rng.integers(0, 2**32, size=100003, dtype=np.uint64).astype(np.uint32)
+    t = torch.from_numpy(w.view(np.int32).copy())
+    for first in (0, 7, 2**40):
+        assert D.bitmap_checksum_tensor(t, first) == D.bitmap_checksum(w, first)

@@ -105,6 +105,22 @@ def test_random_intervals_stats(seed):
     assert np.array_equal(c, oc) and np.array_equal(s, os_)
 
 
+def test_random_intervals_10k_batch_and_single_calls():
+    """SURVEY.md 8(c) random parity: 10^4 seeded intervals, lo uniform in
+    [0, 10^13], width uniform in [0, 10^6] (empty ones included), through
+    sieve_batch, element-wise against oracle.batch; 500 of them also through
+    the single-call path (one fused launch each)."""
+    iv = inputs.random_intervals(10**4, seed=2024, lo_max=10**13, width_max=10**6)
+    lo = np.array([a for a, _ in iv], dtype=np.uint64)
+    hi = np.array([b for _, b in iv], dtype=np.uint64)
+    c, s = sv.batch(lo, hi)
+    oc, os_ = oracle.batch(lo, hi)
+    bad = np.nonzero((c != oc) | (s != os_))[0]
+    assert bad.size == 0, [(int(lo[i]), int(hi[i])) for i in bad[:5]]
+    for k in range(0, 10**4, 20):
+        assert sv.stats(int(lo[k]), int(hi[k])) == (int(oc[k]), int(os_[k])), (int(lo[k]), int(hi[k]))
+
+
 @pytest.mark.parametrize("seg_kb", [32, 64, 128, 192])
 @pytest.mark.parametrize("wheel", [11, 17, 23, 31, 41, 47])
 def test_bitmap_multi_segment_ragged(seg_kb, wheel):
@@ -455,3 +471,36 @@ def test_lifecycle_shutdown_options_streams():
     sv.shutdown()
     lst, n = sv.primes(2, 10**5)
     assert np.array_equal(lst[:n], oracle.primes(2, 10**5))
+
+
+def test_batch_async_device_plan():
+    """A10 planned on the device (sieve_batch_async): device-resident
+    intervals, results element-wise against the oracle; an interval longer
+    than the promised width_max gets the sentinel, the others are unaffected;
+    repeated calls (the class histogram is re-zeroed by each plan)."""
+    torch = pytest.importorskip("torch")
+    iv = inputs.random_intervals(300, seed=77, lo_max=10**13, width_max=3 * 10**6) + [(0, 0), (2, 3), (0, 100)]
+    lo = np.array([a for a, _ in iv], dtype=np.uint64)
+    hi = np.array([b for _, b in iv], dtype=np.uint64)
+    oc, os_ = oracle.batch(lo, hi)
+    dlo = torch.from_numpy(lo.view(np.int64)).cuda()
+    dhi = torch.from_numpy(hi.view(np.int64)).cuda()
+    res = torch.zeros(2 * lo.size, dtype=torch.int64, device="cuda")
+    sv.set_stream(torch.cuda.current_stream())
+    try:
+        for _ in range(3):
+            res.fill_(-7)
+            sv.batch_async(dlo, dhi, int(hi.max()), int((hi - lo).max()), res)
+            torch.cuda.synchronize()
+            got = res.cpu().numpy().view(np.uint64)
+            assert np.array_equal(got[0::2], oc) and np.array_equal(got[1::2], os_)
+        w = int(np.sort(hi - lo)[-2])  # the widest interval exceeds this promise
+        sv.batch_async(dlo, dhi, int(hi.max()), w, res)
+        torch.cuda.synchronize()
+        got = res.cpu().numpy().view(np.uint64)
+        big = int(np.argmax(hi - lo))
+        assert got[2 * big] == got[2 * big + 1] == (1 << 64) - 1
+        keep = np.arange(lo.size) != big
+        assert np.array_equal(got[0::2][keep], oc[keep]) and np.array_equal(got[1::2][keep], os_[keep])
+    finally:
+        sv.set_stream(None)

@@ -61,29 +61,40 @@ def emit(d):
     print(json.dumps(d), flush=True)
 
 
-def config2(opts):
+def config2(opts, lohi=None, tag=2):
+    """Bitmap mode (A7) of config 2 -- or, with lohi = config 3's range, a
+    625 MB bitmap far larger than the 126 MB L2, where HBM binds.  Times:
+    the product call (base primes + sieve + bitmap in one launch,
+    sieve_bitmap_base_async) and the write-back stage in isolation (diagnostic flag 1: wheel init +
+    transpose + count + store, marking skipped)."""
     if isinstance(opts, int):
         opts = {"segment_kb": opts}
     sv.set_options(**opts)
     seg_kb = sv.get_options()
-    lo, hi = inputs.CONFIG2
-    r, b = base_for(hi)
+    lo, hi = lohi or inputs.CONFIG2
+    r = math.isqrt(hi - 1)
+    b = D.alloc_base(sv.base_capacity(r), dev)
     words = sv.bitmap_words(lo, hi)
     out = torch.empty(words, dtype=torch.int32, device=dev)
     res = torch.zeros(2, dtype=torch.int64, device=dev)
-    med, mn = timed(lambda: sv.bitmap_async(lo, hi, b.primes, b.recips, b.nbase, out, res))
-    ok = res.cpu().tolist()[0] == 50847534
+    want = {2: 50847534, 3: 455052511}[tag]
+    med, mn = timed(lambda: sv.bitmap_base_async(lo, hi, b.primes, b.recips, b.nbase, out, res))
+    ok = res.cpu().tolist()[0] == want
     sv.debug_set_flags(1)
-    wmed, wmn = timed(lambda: sv.bitmap_async(lo, hi, b.primes, b.recips, b.nbase, out, res))
+    wmed, wmn = timed(lambda: sv.bitmap_base_async(lo, hi, b.primes, b.recips, b.nbase, out, res))
     sv.debug_set_flags(0)
     byts = words * 4
-    emit({"config": 2, "mode": "bitmap", "segment_kb": seg_kb, "ok": ok, "kernel_ms": med,
+    emit({"config": tag, "mode": "bitmap", "segment_kb": seg_kb, "ok": ok, "kernel_ms": med,
           "integers_per_s": (hi - lo) / (med / 1e3), "bitmap_bytes": byts,
+          "bitmap_vs_l2": "larger than the 126 MB L2" if byts > 126e6 else "fits in L2",
           "hbm_gbs_end_to_end": byts / (med / 1e3) / 1e9,
           "hbm_frac_end_to_end": byts / (med / 1e3) / 1e9 / HBM_PEAK,
           "writeback_only_ms": wmed, "writeback_only_gbs": byts / (wmed / 1e3) / 1e9,
           "writeback_only_frac": byts / (wmed / 1e3) / 1e9 / HBM_PEAK,
-          "hbm_peak_gbs": HBM_PEAK, "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy)"})
+          "hbm_peak_gbs": HBM_PEAK, "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy)",
+          "call": "sieve_bitmap_base_async (fused A2 + sieve + write-back, one launch)"})
+    del out
+    torch.cuda.empty_cache()
     sv.set_options()
 
 
@@ -117,7 +128,7 @@ def config4(seg_kb):
     got = [D.i64_to_u64(x) for x in res.cpu().tolist()]
     emit({"config": 4, "mode": "count+sum", "segment_kb": seg_kb, "kernel_ms": med,
           "integers_per_s": (hi - lo) / (med / 1e3),
-          "ok": got == [361840208, 13161149016643422504]})
+          "ok": got == [361840208, 13161149016643422504], **config4_frac(med, seg_kb)})
     sv.set_options()
 
 
@@ -185,9 +196,44 @@ def f2():
     torch.cuda.empty_cache()
 
 
+def marks_alg_interval(lo: int, hi: int, primes: np.ndarray, wheel: int) -> int:
+    """M_alg of one interval (bench.algorithmic_marks, vectorised): odd
+    multiples m of every prime wheel < p <= isqrt(hi-1), max(lo, p^2) <= m < hi."""
+    if hi <= lo or hi < 10:
+        return 0
+    r = math.isqrt(hi - 1)
+    p = primes[(primes > wheel) & (primes <= r)]
+    a = np.maximum(np.int64(lo), p * p)
+    m0 = (a + p - 1) // p * p
+    m0 = np.where(m0 % 2 == 0, m0 + p, m0)
+    ok = m0 < hi
+    return int((((hi - 1 - m0[ok]) // (2 * p[ok])) + 1).sum())
+
+
+def small_primes_np(r: int) -> np.ndarray:
+    s = np.ones(r + 1, dtype=bool)
+    s[:2] = False
+    for q in range(2, math.isqrt(r) + 1):
+        if s[q]:
+            s[q * q::q] = False
+    return np.nonzero(s)[0].astype(np.int64)
+
+
 def config5():
+    """Config 5 (4096 intervals): kernel-only on device-resident intervals
+    (sieve_batch_async: K1 + the on-device plan + the batch sieve, CUDA
+    events) and end to end through the host API (sieve_batch), with the
+    shared-memory-atomic roofline fraction (M_alg at the build's wheel over
+    all intervals / kernel time / (148 x R_atom x f))."""
     lo, hi = inputs.config5_intervals()
     total = int((hi - lo).sum())
+    hi_max, width_max = int(hi.max()), int((hi - lo).max())
+    dlo = torch.from_numpy(lo.view(np.int64)).to(dev)
+    dhi = torch.from_numpy(hi.view(np.int64)).to(dev)
+    res = torch.zeros(2 * lo.size, dtype=torch.int64, device=dev)
+    med, mn = timed(lambda: sv.batch_async(dlo, dhi, hi_max, width_max, res))
+    got = res.cpu().numpy().view(np.uint64)
+    ok_k = int(got[0::2].sum()) == 715907351
     for _ in range(2):
         c, s = sv.batch(lo, hi)
     ts = []
@@ -195,13 +241,33 @@ def config5():
         t0 = time.perf_counter()
         c, s = sv.batch(lo, hi)
         ts.append(time.perf_counter() - t0)
-    med = statistics.median(ts)
-    emit({"config": 5, "mode": "batch (sieve_batch, host API incl. item upload)", "ms": med * 1e3,
-          "integers_per_s": total / med, "ok": int(c.sum()) == 715907351})
+    e2e = statistics.median(ts)
+    w = sv.get_options()["wheel"]
+    pr = small_primes_np(math.isqrt(hi_max))
+    m_alg = sum(marks_alg_interval(int(a), int(b), pr, w) for a, b in zip(lo, hi))
+    r_atom, _ = sv.debug_k0()
+    peak = 148 * r_atom * 1965e6
+    emit({"config": 5, "mode": "batch", "kernel_ms": med, "kernel_ms_min": mn,
+          "kernel_integers_per_s": total / (med / 1e3), "e2e_ms": e2e * 1e3,
+          "e2e_integers_per_s": total / e2e, "ok": ok_k and int(c.sum()) == 715907351,
+          "kernel_scope": "sieve_batch_async on device-resident intervals: K1 base primes + plan "
+                          "(3 small kernels) + the batch sieve",
+          "e2e_scope": "sieve_batch (host arrays): H2D of the intervals, the same device work, D2H",
+          "wheel": w, "marks_alg": m_alg, "roofline_frac": m_alg / (med / 1e3) / peak,
+          "peak_basis": f"148 x R_atom {r_atom:.2f} (K0) x 1965 MHz"})
+
+
+def config4_frac(kernel_ms: float, seg_kb: int) -> dict:
+    lo, hi = inputs.CONFIG4
+    w = sv.get_options()["wheel"]
+    pr = small_primes_np(math.isqrt(hi - 1))
+    m = marks_alg_interval(lo, hi, pr, w)
+    r_atom, _ = sv.debug_k0()
+    return {"marks_alg": m, "wheel": w, "roofline_frac": m / (kernel_ms / 1e3) / (148 * r_atom * 1965e6)}
 
 
 if __name__ == "__main__":
-    which = [a for a in sys.argv[1:] if "=" not in a] or ["1", "2", "4", "5"]
+    which = [a for a in sys.argv[1:] if "=" not in a] or ["1", "2", "3b", "4", "5"]
     if "1" in which:
         config1()
     if "2" in which:
@@ -212,6 +278,8 @@ if __name__ == "__main__":
         else:
             for kb in (32, 64, 128, 192, 208):
                 config2(kb)
+    if "3b" in which:  # config 3's range in bitmap mode: 625 MB, HBM-bound write-back
+        config2({}, inputs.CONFIG3, tag=3)
     if "4" in which:
         for kb in (32, 208):
             config4(kb)

@@ -29,7 +29,8 @@ for src, dst in [("bench.json", f"{tag}_bench.json"), ("modes.jsonl", f"{tag}_mo
         shutil.copy(os.path.join(SRC, src), os.path.join(DST, dst))
 
 # launch list: keep only the CSV rows, summarise shares per kernel
-lines = [l for l in open(os.path.join(SRC, "launches.csv")) if l.startswith('"')]
+lp = os.path.join(SRC, "launches.csv")
+lines = [l for l in open(lp) if l.startswith('"')] if os.path.exists(lp) else []
 with open(os.path.join(DST, f"{tag}_launches.csv"), "w") as f:
     f.writelines(lines)
 rows = list(csv.DictReader(lines))
@@ -71,17 +72,42 @@ def to_bytes(k):
 
 
 dram = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
+
+# lane-level shared atomics (predicated-on thread instructions of the ATOMS
+# SASS lines, from the source page): the hardware view of the roofline
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+srows = list(csv.reader(src.splitlines()))
+lane_atoms = 0
+if len(srows) > 2:
+    sh = srows[1]
+    i_src, i_th = sh.index("Source"), sh.index("Predicated-On Thread Instructions Executed")
+    for r in srows[2:]:
+        if len(r) > i_th and "ATOMS" in r[i_src]:
+            lane_atoms += int(r[i_th].replace(",", "") or 0)
+cycles = num("sm__cycles_elapsed.avg")
+nsm = 148
+atom = num("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum")
+conf = num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum")
 with open(os.path.join(DST, "ncu_sieve_summary.json"), "w") as f:
     json.dump({"tag": tag, "kernel": m.get("Kernel Name"), "dram_bytes_per_launch": dram,
-               "source": "ncu --set full --clock-control none, one launch of bench.py config 3"}, f, indent=1)
+               "lane_atomics_per_launch": lane_atoms,
+               "atomic_lane_util": lane_atoms / (nsm * 32 * cycles) if cycles == cycles and cycles else None,
+               "smem_pipe_pct": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+               "atomic_wavefronts_per_instr": atom / max(atom - conf, 1),
+               "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+               "sm_cycles": cycles,
+               "source": "ncu --set full --clock-control none, one launch of bench.py config 3; "
+                         "atomic_lane_util = predicated-on ATOMS thread instructions / "
+                         "(148 SMs x 32 lanes x SM cycles)"}, f, indent=1)
 
 with open(os.path.join(DST, f"{tag}_ncu_sieve.txt"), "w") as f:
     f.write(f"# ncu --set full capture of the sieve kernel ({tag}); bench.py --steps 1 --warmup 0\n")
     for k in keys:
         f.write(f"{k} = {m.get(k)} {units.get(k, '')}\n")
-    atom = num("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum")
-    conf = num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum")
     f.write(f"atomic wavefronts per atomic instruction = {atom / max(atom - conf, 1):.3f}\n")
+    f.write(f"lane atomics (predicated-on ATOMS thread instructions) = {lane_atoms}\n")
+    f.write(f"atomic lane utilisation = {lane_atoms / (nsm * 32 * cycles):.3f} of 148 x 32 lanes x cycles\n")
     f.write(f"dram bytes per launch = {dram:.0f}\n")
     f.write("\n# launch list shares (ncu, cold-cache, serialised)\n")
     for k, (n, ns) in sorted(tot.items(), key=lambda x: -x[1][1]):

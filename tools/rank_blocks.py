@@ -11,7 +11,9 @@ from paper_1205_4883_b200 import dist as D
 stream = torch.cuda.Stream(); sv.set_stream(stream); torch.cuda.set_stream(stream)
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 lo, hi = bench.CONFIG3
-peak = 148 * bench.SMEM_LANES_PER_CLK * 1965e6 / 1e9
+r_atom, _ = sv.debug_k0()  # K0 on this GPU (lanes/clk/SM)
+peak = 148 * r_atom * 1965e6 / 1e9
+W = sv.get_options()["wheel"]
 for G in [int(x) for x in os.environ.get("GS", "1,2,4,8").split(",")]:
     for g in sorted({0, G - 1}):
         a, b = D.block_of(lo, hi, g, G)
@@ -36,7 +38,7 @@ for G in [int(x) for x in os.environ.get("GS", "1,2,4,8").split(",")]:
             if i >= 3:
                 fs.append(e[0].elapsed_time(e[1]))
         k = statistics.median(ks)
-        m = bench.algorithmic_marks(a, b)
+        m = bench.algorithmic_marks(a, b, W)
         print(f"G={G} rank={g} [{a},{b}) K1={statistics.median(bs)*1e3:.1f}us sieve={k*1e3:.1f}us "
               f"frac={m / (k / 1e3) / 1e9 / peak:.3f} | K1+sieve={(statistics.median(bs) + k)*1e3:.1f}us "
               f"fused={statistics.median(fs)*1e3:.1f}us", flush=True)
