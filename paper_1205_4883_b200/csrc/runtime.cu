@@ -226,11 +226,21 @@ int ensure_ready() {
   return 0;
 }
 
-size_t seg_bits() { return (size_t)g.opt.segment_kb * 8192; }
+// options not set yet (a call may plan before ensure_ready): the defaults
+void ensure_options() {
+  if (g.opt.segment_kb == 0) default_options(g.opt);
+}
+size_t seg_bits() {
+  ensure_options();
+  return (size_t)g.opt.segment_kb * 8192;
+}
 size_t smem_for(uint32_t segment_kb, uint32_t wheel) {
   return (size_t)segment_kb * 1024 + sv::tables_words(ng_for_wheel(wheel)) * 4 + sv::kSmemAlign;
 }
-size_t sieve_smem() { return smem_for(g.opt.segment_kb, g.opt.wheel); }
+size_t sieve_smem() {
+  ensure_options();
+  return smem_for(g.opt.segment_kb, g.opt.wheel);
+}
 
 int ensure_smem_attr() {
   const size_t sm = sieve_smem();

@@ -62,3 +62,21 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(sv.SieveError) as e:
         sv.count(2, 100)
     assert e.value.code == -5
+
+
+def test_planning_before_any_option_call():
+    """A device-resident call made before any set_options/sync call plans
+    with the default options (it used to divide by a zero segment size):
+    without a GPU it must fail with SIEVE_ENODEV or SIEVE_EINVAL, not crash."""
+    import subprocess
+    import sys
+    code = ("import paper_1205_4883_b200 as sv, torch\n"
+            "try:\n"
+            "    sv.lib().sieve_stats_base_async(2, 10**10 + 1, 1, 1, 1, 10**6, 0, 1)\n"
+            "except Exception as e:\n"
+            "    print(e)\n"
+            "print('alive', sv.lib().sieve_stats_base_async(2, 10**10 + 1, 1, 1, 1, 10**6, 0, 1))\n")
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert p.returncode == 0, p.stderr
+    assert "alive" in p.stdout
