@@ -88,6 +88,10 @@ constexpr uint32_t kC15Hits = SIEVE_C15_HITS;
 #define SIEVE_PLAIN_HITS 8  // A/B on config 5: 2 -> 6.49, 4 -> 6.40, 8 -> 6.34, 16 -> 6.37, 32 -> 6.40 ms
 #endif
 constexpr uint32_t kPlainHits = SIEVE_PLAIN_HITS;
+#ifndef SIEVE_PLAIN_ILP  // batch kernel: plain primes per thread and pass
+#define SIEVE_PLAIN_ILP 8  // config 5: 2 -> 5.39, 4 -> 5.13, 8 -> 5.07 ms
+#endif
+constexpr int kPlainILP = SIEVE_PLAIN_ILP;
 #ifndef SIEVE_BUCKET_HITS
 #define SIEVE_BUCKET_HITS 1
 #endif

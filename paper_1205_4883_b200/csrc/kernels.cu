@@ -73,6 +73,16 @@ __device__ __forceinline__ uint32_t first_hit(uint64_t a, uint64_t seg_end, uint
   return pp >= seg_end ? kNone : j;
 }
 
+// first_hit when p^2 <= a (the segment lies above p^2): the first odd multiple
+// a + 2 j of p, r = a mod p by the same Barrett step, j = (((r & 1) ? p : 2 p)
+// - r) / 2 mod p (a odd: r odd leaves p - r even).  No clamp, no 64-bit compare.
+__device__ __forceinline__ uint32_t first_hit_above(uint64_t a, uint32_t p, uint64_t recip) {
+  uint32_t r = (uint32_t)a - (uint32_t)__umul64hi(a, recip) * p;
+  r = min(r, r - p);  // a mod p
+  const uint32_t j = (((r & 1u) ? p : 2u * p) - r) >> 1;
+  return min(j, j - p);  // r = 0: j = p -> 0
+}
+
 // floor((2^64-1)/p) for an odd p >= 3, without a 64-bit integer division:
 // a double quotient (within 2^12 of the result), then the exact remainder
 // T = (2^64-1) - q p (|T| < 2^40, so mod-2^64 arithmetic gives it as a signed
@@ -545,29 +555,42 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // out of the other kernels, whose loops it would perturb (+0.7 % measured)
   const uint32_t two = kPlainTwo ? max(few, min(R.two, c_end)) : c_end;
   c_loop(few, two, std::false_type{});
-  if constexpr (kPlainTwo)
-  for (uint32_t k0 = two; k0 < c_end; k0 += kLargeILP * blockDim.x) {
-    uint32_t pk[kLargeILP], jk[kLargeILP];
-    uint64_t rk[kLargeILP];
+  // The plain primes (batch kernel): kPlainILP per thread and pass.  While
+  // the pass's largest prime has p^2 <= a (the item lies above p^2 -- almost
+  // always in a batch far from 0), the first hit needs neither the p^2 clamp
+  // nor the 64-bit compares of first_hit: with r = a mod p (Barrett), the
+  // first odd multiple a + 2 j has j = (((r & 1) ? p : 2 p) - r) / 2 mod p.
+  // (Config 5 spends most of its time here: one such reduction per (prime,
+  // item) for ~1.1e9 pairs, most of them without a hit.)
+  if constexpr (kPlainTwo) {
+    constexpr int U = kPlainILP;
+    for (uint32_t k0 = two; k0 < c_end; k0 += U * blockDim.x) {
+      uint32_t pk[U], jk[U], kk[U];
+      uint64_t rk[U];
 #pragma unroll
-    for (int u = 0; u < kLargeILP; ++u) {
-      const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
-      const uint32_t k = min(ku, c_end - 1u);
-      pk[u] = __ldg(primes + k);
-      rk[u] = __ldg(recips + k);
-    }
+      for (int u = 0; u < U; ++u) {
+        kk[u] = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+        const uint32_t k = min(kk[u], c_end - 1u);
+        pk[u] = __ldg(primes + k);
+        rk[u] = __ldg(recips + k);
+      }
+      if ((uint64_t)pk[U - 1] * pk[U - 1] <= a) {  // the largest of the pass: so for all
 #pragma unroll
-    for (int u = 0; u < kLargeILP; ++u) {
-      jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
-      const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
-      if (ku >= c_end) jk[u] = kNone;
-    }
-    if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
+        for (int u = 0; u < U; ++u) jk[u] = kk[u] < c_end ? first_hit_above(a, pk[u], rk[u]) : kNone;
+      } else {
 #pragma unroll
-    for (int u = 0; u < kLargeILP; ++u) {
-      if (jk[u] == kNone) break;
-      const uint32_t P4 = 4u * pk[u];
-      for (uint32_t J = 4u * jk[u] + 32u * sb; J < Jlim; J += P4) red_or(j_addr(J), j_mask(J));
+        for (int u = 0; u < U; ++u) {
+          jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
+          if (kk[u] >= c_end) jk[u] = kNone;
+        }
+        if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (jk[u] == kNone) break;  // past c_end (or p^2 past the segment), and so the later ones
+        const uint32_t P4 = 4u * pk[u];
+        for (uint32_t J = 4u * jk[u] + 32u * sb; J < Jlim; J += P4) red_or(j_addr(J), j_mask(J));
+      }
     }
   }
   if (prof) {  // per-warp busy cycles of the regions (diagnostics only)
