@@ -262,7 +262,10 @@ int sieve_debug_set_profile(uint64_t *dev_counters);
  * these is set.  16 = every CTA walks its segments in reverse order (bitmap
  * mode; schedule invariance: results must not change); 32 = never use the cooperative fused-A2 launch (the K1 + ordinary
  * launch path the library falls back to when a cooperative launch is
- * refused; results must not change).  0 restores. */
+ * refused; results must not change); 64 = count mode through the F3
+ * cluster-pair kernel (two CTAs per super-segment, the large primes over
+ * distributed shared memory; an A/B variant, results must not change).
+ * 0 restores. */
 int sieve_debug_set_flags(uint32_t flags);
 
 /* Diagnostics (bounds-check build, `make check` -> libsieve_check.so,

@@ -368,7 +368,7 @@ def kernel_launches() -> int:
 
 
 FLAG_SKIP_MARKING, FLAG_SKIP_A, FLAG_SKIP_B, FLAG_SKIP_C = 1, 2, 4, 8
-FLAG_REVERSE, FLAG_NO_COOP = 16, 32
+FLAG_REVERSE, FLAG_NO_COOP, FLAG_CLUSTER = 16, 32, 64
 
 
 def debug_violations(reset: bool = False) -> tuple[bool, list[int]]:

@@ -232,6 +232,10 @@ constexpr uint32_t kFlagReverse = 16u;
 // Diagnostic flag: never take the cooperative (fused A2) launch -- the path
 // the runtime falls back to when a cooperative launch is refused.
 constexpr uint32_t kFlagNoCoop = 32u;
+// Diagnostic flag (count mode, F3): the cluster-pair kernel k_sieve_cluster
+// (two CTAs per super-segment, region C over distributed shared memory), base
+// primes by K1.  An A/B variant, not the product path.
+constexpr uint32_t kFlagCluster = 64u;
 
 enum Mode { kCount = 0, kBitmap = 1, kBatch = 2, kList = 3 };
 
@@ -242,6 +246,8 @@ constexpr uint64_t kMaxSmallWords = 1024;
 cudaError_t launch_sieve(int ng, int mode, const SieveParams &p, int grid, int threads,
                          size_t smem, cudaStream_t s);
 cudaError_t set_sieve_smem_limits(size_t smem);
+cudaError_t launch_sieve_cluster(int ng, const SieveParams &p, int grid, int threads, size_t smem,
+                                 cudaStream_t s);
 cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64_t *recips,
                                uint32_t cap, uint32_t *nbase, uint64_t *flags, uint32_t epoch,
                                int nsm, unsigned long long *prof, cudaStream_t s);

@@ -1616,6 +1616,131 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
 }
 
 // ---------------------------------------------------------------------------
+// F3: the paper's "bidirectional" sieve of one deque by two
+// workers (Alg. 1) re-expressed as a thread-block CLUSTER
+// of two CTAs (two SMs) sieving one super-segment of 2 S slots: CTA rank r
+// holds half r (its own shared-memory segment, as in k_sieve).  Small and
+// medium primes (regions A, B) are marked by each CTA in its own half.  The
+// large primes (region C, lane per prime) are split between the two CTAs and
+// each is walked ONCE over the whole super-segment: one first-hit reduction
+// per prime and super-segment instead of per segment, and walks twice as
+// long; a hit in the partner's half is a distributed-shared-memory atomic
+// (mapa + red.shared::cluster).  Two cluster barriers per super-segment: both
+// halves initialised before any mark, every mark (local and remote) done
+// before either epilogue.  Count mode only, base primes from K1; a
+// diagnostics variant for the A/B of DESIGN.md (kFlagCluster), not the
+// product path: DSMEM atomics run at a fraction of local ones
+// (profiles/r01_micro_pipes.json), which this kernel measures in context.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// OR into the partner CTA's segment at the same shared-window offset
+__device__ __forceinline__ void red_or_remote(uint32_t saddr, uint32_t rank, uint32_t mask) {
+#if SIEVE_CHECK_BOUNDS
+  SV_CHECK(saddr >= s_chk_lo && saddr < s_chk_hi && __popc(mask) == 1, kVioSmemMark);
+#endif
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(saddr), "r"(rank));
+  asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(ra), "r"(mask) : "memory");
+}
+
+template <int NG>
+__global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve_cluster(const SieveParams P) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const uint32_t sraw = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t sb = (sraw + (kSmemAlign - 1u)) & ~(kSmemAlign - 1u);
+  uint32_t *seg = smem + (sb - sraw) / 4u;
+  uint32_t *tab = seg + P.seg_bits / 32;
+  __shared__ unsigned long long red[64];
+  __shared__ PrimeRegions sR;
+  __shared__ uint32_t s_last;
+  __shared__ uint32_t s_ub[7];
+  __shared__ uint32_t s_k15[15];
+#if SIEVE_CHECK_BOUNDS
+  if (threadIdx.x == 0) {
+    s_chk_lo = sb;
+    s_chk_hi = sb + P.seg_bits / 8u;
+  }
+#endif
+  if (threadIdx.x < 15u) s_k15[threadIdx.x] = kept15(threadIdx.x / 5u, threadIdx.x % 5u);
+  for (uint32_t i = threadIdx.x; i < tables_words(NG); i += blockDim.x) tab[i] = P.tables[i];
+  compute_regions(P, P.r, sR, s_ub, wheel_nprimes(NG), false);
+  __syncthreads();
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t ncl = gridDim.x >> 1, cid = blockIdx.x >> 1;
+  const uint32_t S = P.seg_bits;
+  const PrimeRegions R = sR;
+  unsigned long long cnt = 0, sum = 0;
+  for (uint64_t u = cid; 2u * u < P.nseg; u += ncl) {
+    const uint64_t s = 2u * u + rank;
+    auto valid_of = [&](uint64_t x) -> uint32_t {
+      if (x >= P.nseg) return 0u;
+      const uint64_t left = P.nbits - x * S;
+      return left < S ? (uint32_t)left : S;
+    };
+    const uint32_t valid = valid_of(s), V = valid_of(2u * u) + valid_of(2u * u + 1u);
+    const uint64_t a = P.o0 + 2ull * s * S;          // this half's first odd integer
+    const uint64_t a0 = P.o0 + 4ull * u * S;         // the super-segment's
+    if (valid) wheel_init<NG, 1>(seg, tab, P.o0, s * (uint64_t)S, valid, a);
+    cluster_sync_all();  // both halves initialised before any mark
+    if (valid) mark_segment<false>(sb, P.primes, P.recips, R, P.flags | kFlagSkipC, a, valid, nullptr, s_k15);
+    // region C over the super-segment, primes split between the two CTAs:
+    // cluster thread T = rank nt + t takes primes R.warp + T + 2 nt m
+    {
+      const uint64_t send = a0 + 2ull * V;
+      const uint32_t a3 = (uint32_t)(a0 % 3u);
+      const uint32_t nt = blockDim.x, T = rank * nt + threadIdx.x;
+      for (uint32_t k = R.warp + T; k < R.end; k += 2u * nt) {
+        const uint32_t p = __ldg(P.primes + k);
+        const uint32_t j0 = first_hit(a0, send, p, __ldg(P.recips + k));
+        if (j0 == kNone) break;  // p^2 past the super-segment: so for every later prime
+        const uint32_t r0 = skip_residue(a3, j0, p);  // hits k = r0 (mod 3): multiples of 3
+        uint32_t j1 = j0 + keep_lo(r0) * p, j2 = j0 + keep_hi(r0) * p;
+        const uint32_t p3 = 3u * p;
+        for (; j1 < V; j1 += p3, j2 += p3) {
+          const uint32_t o1 = j1 >= S ? 1u : 0u, l1 = j1 - o1 * S;
+          if (o1 == rank) red_or(sb + t_addr(l1), t_mask(l1)); else red_or_remote(sb + t_addr(l1), o1, t_mask(l1));
+          if (j2 < V) {
+            const uint32_t o2 = j2 >= S ? 1u : 0u, l2 = j2 - o2 * S;
+            if (o2 == rank) red_or(sb + t_addr(l2), t_mask(l2)); else red_or_remote(sb + t_addr(l2), o2, t_mask(l2));
+          }
+        }
+      }
+    }
+    cluster_sync_all();  // every mark of both halves done
+    if (valid) epilogue<kCount>(seg, a, s * (uint64_t)S, valid, nullptr, 0, 0, cnt, sum);
+    __syncthreads();
+  }
+  block_sum2(cnt, sum, red);
+  if (threadIdx.x == 0) {
+    unsigned long long *acc = reinterpret_cast<unsigned long long *>(P.partials);
+    atomicAdd(acc, cnt);
+    atomicAdd(acc + 1, sum);
+    __threadfence();
+    const unsigned int t = atomicAdd(P.done, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    unsigned long long *acc = reinterpret_cast<unsigned long long *>(P.partials);
+    unsigned long long c = atomicExch(acc, 0ull), sm = atomicExch(acc + 1, 0ull);
+    if (P.add_two) { c += 1; sm += 2; }
+    P.result[0] = c;
+    P.result[1] = sm;
+    *P.done = 0u;
+  }
+  cluster_sync_all();  // no CTA leaves while its partner may still address its shared memory
+}
+
+// ---------------------------------------------------------------------------
 // A2: base primes, the odd primes <= r (r <= 2^24), ascending, with their
 // Barrett reciprocals.  The odd numbers n = 2i + 1 <= r (i >= 1) are cut into
 // slices of kSliceBits; a CTA of kBaseThreads threads takes slices b, b + G,
@@ -1884,6 +2009,38 @@ static cudaError_t launch_m(int ng, const SieveParams &p, int grid, int threads,
     case 4: return launch_t<4, MODE>(p, grid, threads, smem, s);
     case 5: return launch_t<5, MODE>(p, grid, threads, smem, s);
     case 6: return launch_t<6, MODE>(p, grid, threads, smem, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int NG>
+static cudaError_t launch_cluster_t(const SieveParams &p, int grid, int threads, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k_sieve_cluster<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(grid & ~1));
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_sieve_cluster<NG>, p);
+}
+
+cudaError_t launch_sieve_cluster(int ng, const SieveParams &p, int grid, int threads, size_t smem,
+                                 cudaStream_t s) {
+  switch (ng) {
+    case 1: return launch_cluster_t<1>(p, grid, threads, smem, s);
+    case 2: return launch_cluster_t<2>(p, grid, threads, smem, s);
+    case 3: return launch_cluster_t<3>(p, grid, threads, smem, s);
+    case 4: return launch_cluster_t<4>(p, grid, threads, smem, s);
+    case 5: return launch_cluster_t<5>(p, grid, threads, smem, s);
+    case 6: return launch_cluster_t<6>(p, grid, threads, smem, s);
     default: return cudaErrorInvalidValue;
   }
 }

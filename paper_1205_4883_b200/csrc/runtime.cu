@@ -418,7 +418,7 @@ struct BaseReq {
 // primes staged for emission (<= L/3 + 2: one of three consecutive odd
 // numbers is a multiple of 3)
 bool fused_fits(uint64_t r, int grid, uint64_t sbits) {
-  if (g.flags & sv::kFlagNoCoop) return false;       // diagnostics: the K1 + ordinary-launch path
+  if (g.flags & (sv::kFlagNoCoop | sv::kFlagCluster)) return false;  // diagnostics: K1 + an ordinary launch
   if (grid > g.nsm * occupancy()) return false;      // not co-resident (grid_for clamps: never)
   const uint64_t imax = r >= 3 ? (r - 1) / 2 : 0;
   const uint64_t L = ((imax + grid - 1) / grid + 31) / 32 * 32;
@@ -463,6 +463,12 @@ int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork, const BaseReq *req =
       g_coop_fallbacks += 1;
     }
     TRY(base_primes(req->r, req->primes, req->recips, req->cap, req->nbase, g.stream()));
+  }
+  if (mode == sv::kCount && (g.flags & sv::kFlagCluster) && !sp.peers && !sp.buckets && grid >= 2) {
+    // F3 diagnostics: the cluster-pair kernel (two CTAs per super-segment)
+    CUDA_TRY(sv::launch_sieve_cluster(ng, sp, grid, (int)g.opt.threads, sieve_smem(), g.stream()));
+    g_launches += 1;
+    return 0;
   }
   CUDA_TRY(sv::launch_sieve(ng, mode, sp, grid, (int)g.opt.threads, sieve_smem(), g.stream()));
   g_launches += 1;
@@ -1141,7 +1147,7 @@ int sieve_is_prime(const uint64_t *nums, uint64_t n, uint8_t *out) {
 int sieve_debug_set_flags(uint32_t flags) {
   std::lock_guard<std::mutex> lk(g.mu);
   if (flags & ~(sv::kFlagSkipMarking | sv::kFlagSkipA | sv::kFlagSkipB | sv::kFlagSkipC |
-                sv::kFlagReverse | sv::kFlagNoCoop))
+                sv::kFlagReverse | sv::kFlagNoCoop | sv::kFlagCluster))
     return fail(SIEVE_EINVAL, "unknown debug flags %u", flags);
   g.flags = flags;
   return 0;

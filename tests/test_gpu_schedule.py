@@ -97,3 +97,20 @@ def test_k0_conflict_free_atomic_rate():
     lanes, ghz = sv.debug_k0()
     assert 28.0 < lanes <= 32.5, lanes
     assert 0.5 < ghz < 2.2, ghz
+
+
+@pytest.mark.parametrize("seg_kb", [16, 32, 208])
+def test_f3_cluster_pair_kernel_parity(seg_kb):
+    """F3 (PAPER.md:137-161 re-expressed): the cluster-pair
+    kernel -- two CTAs per super-segment, the large primes walked once over
+    both halves, the partner half marked through distributed shared memory --
+    gives the oracle's results (odd and even segment counts, ragged ends,
+    first segments below p^2).  It is a measured A/B variant (3-6x slower,
+    profiles/r02_f3_cluster_ab.jsonl), not the product path."""
+    sv.set_options(segment_kb=seg_kb)
+    sv.debug_set_flags(64)  # FLAG_CLUSTER
+    for lo, hi in [(2, 10**8 + 1), (10**12 + 1, 10**12 + 3 * 10**7 + 7), (999_999_999_989, 1_000_040_000_000),
+                   (0, 5000), (3, 10**6)]:
+        assert sv.stats(lo, hi) == oracle.stats(lo, hi), (lo, hi, seg_kb)
+    if seg_kb == 208:
+        assert sv.stats(*inputs.CONFIG3) == (455052511, 2220822432581729238)

@@ -48,7 +48,7 @@ for o in opts:
         three_modes(lo, hi)
 sv.set_options()
 # diagnostic paths: reversed segment order, the non-cooperative fallback
-for flags in (sv.FLAG_REVERSE, sv.FLAG_NO_COOP, sv.FLAG_REVERSE | sv.FLAG_NO_COOP):
+for flags in (sv.FLAG_REVERSE, sv.FLAG_NO_COOP, sv.FLAG_REVERSE | sv.FLAG_NO_COOP, sv.FLAG_CLUSTER):
     sv.debug_set_flags(flags)
     for lo, hi in ranges[:5]:
         three_modes(lo, hi)
