@@ -57,8 +57,56 @@ def base_for(hi):
     return r, b
 
 
+RESULTS = []
+
+
 def emit(d):
+    RESULTS.append(d)
     print(json.dumps(d), flush=True)
+
+
+def oracle_report(path):
+    """SURVEY.md 8(d) D4 / BASELINE.md 5: the oracle on the host cores per
+    config (T = all hardware threads; T = 1 for configs 1-2), next to the GPU
+    numbers of this run, with nproc and the CPU model -> report.json."""
+    import oracle
+    import bench
+
+    T = oracle.default_threads()
+
+    def t(fn):
+        t0 = time.perf_counter()
+        out = fn()
+        return time.perf_counter() - t0, out
+
+    rep = {"host": {**bench.host_cpu(), "threads": T}, "gpu": RESULTS, "oracle": {}}
+    o = rep["oracle"]
+    lo, hi = inputs.CONFIG1
+    for th in (T, 1):
+        ds, _ = t(lambda: (oracle.stats(lo, hi, th), oracle.primes(lo, hi, threads=th),
+                           oracle.bitmap(lo, hi, th)))
+        o[f"config1_T{th}"] = {"s": ds, "what": "count+sum, list, bitmap of [2, 1e7+1)"}
+    lo, hi = inputs.CONFIG2
+    for th in (T, 1):
+        ds, (bm, c, _) = t(lambda: oracle.bitmap(lo, hi, th))
+        o[f"config2_T{th}"] = {"s": ds, "what": "bitmap + count + sum of [2, 1e9+1)",
+                               "ok": c == 50847534 and oracle.fnv1a64(bm) == 0xe4b98535dc2fea3d}
+    lo, hi = inputs.CONFIG3
+    ds, r = t(lambda: oracle.stats(lo, hi, T))
+    o[f"config3_T{T}"] = {"s": ds, "what": "count+sum of [2, 1e10+1)",
+                          "ok": r == (455052511, 2220822432581729238)}
+    lo, hi = inputs.CONFIG4
+    ds, r = t(lambda: oracle.stats(lo, hi, T))
+    o[f"config4_T{T}"] = {"s": ds, "what": "count+sum of the whole window [1e12, 1e12+1e10)",
+                          "ok": r == (361840208, 13161149016643422504)}
+    ds, _ = t(lambda: [oracle.primes(a, b, threads=T) for a, b in inputs.config4_subwindows()])
+    o[f"config4_subwindows_T{T}"] = {"s": ds, "what": "the 16 sub-window lists (width 1e7)"}
+    l5, h5 = inputs.config5_intervals()
+    ds, (c5, _) = t(lambda: oracle.batch(l5, h5, T))
+    o[f"config5_T{T}"] = {"s": ds, "what": "all 4096 intervals, count+sum", "ok": int(c5.sum()) == 715907351}
+    with open(path, "w") as f:
+        json.dump(rep, f, indent=1)
+    print(json.dumps({"report": path, "oracle": o}), flush=True)
 
 
 def config2(opts, lohi=None, tag=2):
@@ -267,11 +315,11 @@ def config4_frac(kernel_ms: float, seg_kb: int) -> dict:
 
 
 if __name__ == "__main__":
-    which = [a for a in sys.argv[1:] if "=" not in a] or ["1", "2", "3b", "4", "5"]
+    which = [a for a in sys.argv[1:] if "=" not in a and not a.startswith("--")] or ["1", "2", "3b", "4", "5"]
     if "1" in which:
         config1()
     if "2" in which:
-        specs = [a for a in sys.argv[1:] if "=" in a]
+        specs = [a for a in sys.argv[1:] if "=" in a and not a.startswith("--")]
         if specs:
             for spec in specs:
                 config2({k: int(v) for k, v in (kv.split("=") for kv in spec.split(","))})
@@ -288,3 +336,6 @@ if __name__ == "__main__":
         config5()
     if "f2" in which:
         f2()
+    rp = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--report=")]
+    if rp:
+        oracle_report(rp[0])

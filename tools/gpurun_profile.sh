@@ -1,11 +1,15 @@
-# Round profiling pass (run under gpurun): GPU tests, bench, modes, K0, the
-# ncu launch list and one `--set full` capture of the sieve kernel.
+# Round profiling pass (run under gpurun): GPU tests, bench, modes + oracle
+# report, K0, per-rank blocks, F3 A/B, phase counters, the ncu launch list and
+# one `--set full` capture of the sieve kernel.
 # tools/make_profile_summary.py <tag> turns gpurun_out/ into profiles/.
 set -x
 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -5 gpurun_out/pytest_gpu.log
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
-python tools/bench_modes.py > gpurun_out/modes.jsonl 2> gpurun_out/modes.err; cat gpurun_out/modes.jsonl; tail -3 gpurun_out/modes.err
-./build/k0_peaks > gpurun_out/k0.json; cat gpurun_out/k0.json
+python tools/bench_modes.py --report=gpurun_out/report.json > gpurun_out/modes.jsonl 2> gpurun_out/modes.err; cat gpurun_out/modes.jsonl; tail -3 gpurun_out/modes.err
+make build/k0_peaks > /dev/null 2>&1; ./build/k0_peaks > gpurun_out/k0.json; cat gpurun_out/k0.json
+python tools/rank_blocks.py > gpurun_out/rank_blocks.txt 2>&1; cat gpurun_out/rank_blocks.txt
+python tools/f3_ab.py > gpurun_out/f3_ab.jsonl 2>&1; cat gpurun_out/f3_ab.jsonl
+python tools/phase_prof.py > gpurun_out/phase.json 2>&1
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
 python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_sieve -c 1 -o gpurun_out/prof_sieve python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out

@@ -24,7 +24,9 @@ rep = os.path.join(SRC, sys.argv[2] if len(sys.argv) > 2 else "prof_sieve.ncu-re
 os.makedirs(DST, exist_ok=True)
 
 for src, dst in [("bench.json", f"{tag}_bench.json"), ("modes.jsonl", f"{tag}_modes.jsonl"),
-                 ("k0.json", f"{tag}_k0_peaks.json")]:
+                 ("k0.json", f"{tag}_k0_peaks.json"), ("report.json", f"{tag}_report.json"),
+                 ("rank_blocks.txt", f"{tag}_rank_blocks.txt"), ("f3_ab.jsonl", f"{tag}_f3_cluster_ab.jsonl"),
+                 ("phase.json", f"{tag}_phase_counters.json"), ("pytest_gpu.log", f"{tag}_pytest_gpu.log")]:
     if os.path.exists(os.path.join(SRC, src)):
         shutil.copy(os.path.join(SRC, src), os.path.join(DST, dst))
 
