@@ -92,6 +92,16 @@ constexpr uint32_t kPlainHits = SIEVE_PLAIN_HITS;
 #define SIEVE_PLAIN_ILP 8  // config 5: 2 -> 5.39, 4 -> 5.13, 8 -> 5.07 ms
 #endif
 constexpr int kPlainILP = SIEVE_PLAIN_ILP;
+#ifndef SIEVE_PLAIN_ILP_COUNT  // the same pass in the count/bitmap/list kernels of large r
+#define SIEVE_PLAIN_ILP_COUNT 8  // config 4: 2 -> 1.782, 4 -> 1.761, 8 -> 1.751 ms
+#endif
+#ifndef SIEVE_PLAIN_NG  // the wheel (groups) for which the plain-pass kernels are instantiated
+#define SIEVE_PLAIN_NG 4
+#endif
+constexpr int kPlainILPCount = SIEVE_PLAIN_ILP_COUNT;
+#ifndef SIEVE_COUNT_PLAIN  // count mode with r > S / kPlainHits: the plain-prime pass (k_sieve<.., kCount, true>)
+#define SIEVE_COUNT_PLAIN 1
+#endif
 #ifndef SIEVE_BUCKET_HITS
 #define SIEVE_BUCKET_HITS 1
 #endif

@@ -336,12 +336,13 @@ __device__ __forceinline__ uint32_t class_limit(uint32_t j, uint32_t valid) {
 // broadcast; p^2 >= segment end stops a warp.  Work is dealt statically and
 // evenly: (A2) in pieces round robin, (B) and (C) in boustrophedon order over
 // the warps / threads.
-template <bool kPlainTwo>
+template <int kPlainU>  // primes per thread and pass of the plain loop; 0 = no plain loop
 __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__restrict__ primes,
                                              const uint64_t *__restrict__ recips,
                                              const PrimeRegions R, uint32_t flags,
                                              uint64_t a, uint32_t valid, unsigned long long *prof,
                                              const uint32_t *k15) {
+  constexpr bool kPlainTwo = kPlainU > 0;
   // diagnostics (sieve_debug_set_flags): drop whole regions (wrong results)
   const uint32_t a1_end = flags & kFlagSkipA ? R.start : R.unit;
   const uint32_t a2_end = flags & kFlagSkipA ? R.unit : R.cls;
@@ -563,7 +564,7 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // (Config 5 spends most of its time here: one such reduction per (prime,
   // item) for ~1.1e9 pairs, most of them without a hit.)
   if constexpr (kPlainTwo) {
-    constexpr int U = kPlainILP;
+    constexpr int U = kPlainU > 0 ? kPlainU : 1;
     for (uint32_t k0 = two; k0 < c_end; k0 += U * blockDim.x) {
       uint32_t pk[U], jk[U], kk[U];
       uint64_t rk[U];
@@ -1409,7 +1410,13 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
 // count/write-back), so nothing but the bitmap (bitmap mode) and 16 bytes per
 // CTA ever reach HBM.
 // ---------------------------------------------------------------------------
-template <int NG, int MODE>
+// kPlain: the plain-prime pass of the batch kernel (primes with at most
+// kPlainHits hits per segment: clamp-free first hits, several per thread and
+// pass) compiled into the count, bitmap and list kernels too, chosen at
+// launch when such primes exist (r > S / kPlainHits: config 4) -- a separate
+// instantiation, so that the kernels of small r (config 3) keep their code
+// generation.  Config 4: 1.931 -> 1.751 ms (same-box A/B).
+template <int NG, int MODE, bool kPlain = false>
 __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   constexpr int kWheelUnrollOf = MODE == kCount ? kWheelUnroll : 1;
@@ -1531,7 +1538,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     if (!(pre_init && s_it == s_begin)) wheel_init<NG, kWheelUnrollOf>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
-    if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);
+    if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch ? kPlainILP : kPlain ? kPlainILPCount : 0>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);
     if (buckets) {
       bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s_it), valid);
       bq = bq + 1u == P.ring ? 0u : bq + 1u;
@@ -1690,7 +1697,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve_cluster(const Si
     const uint64_t a0 = P.o0 + 4ull * u * S;         // the super-segment's
     if (valid) wheel_init<NG, 1>(seg, tab, P.o0, s * (uint64_t)S, valid, a);
     cluster_sync_all();  // both halves initialised before any mark
-    if (valid) mark_segment<false>(sb, P.primes, P.recips, R, P.flags | kFlagSkipC, a, valid, nullptr, s_k15);
+    if (valid) mark_segment<0>(sb, P.primes, P.recips, R, P.flags | kFlagSkipC, a, valid, nullptr, s_k15);
     // region C over the super-segment, primes split between the two CTAs:
     // cluster thread T = rank nt + t takes primes R.warp + T + 2 nt m
     {
@@ -1980,8 +1987,8 @@ cudaError_t launch_batch_plan(const uint64_t *lo, const uint64_t *hi, uint64_t n
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-template <int NG, int MODE>
-static cudaError_t launch_t(const SieveParams &p, int grid, int threads, size_t smem, cudaStream_t s) {
+template <int NG, int MODE, bool kPlain = false>
+static cudaError_t launch_tp(const SieveParams &p, int grid, int threads, size_t smem, cudaStream_t s) {
   if (p.bprimes) {  // fused A2: grid barriers need every CTA resident
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -1993,10 +2000,20 @@ static cudaError_t launch_t(const SieveParams &p, int grid, int threads, size_t 
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_sieve<NG, MODE>, p);
+    return cudaLaunchKernelEx(&cfg, k_sieve<NG, MODE, kPlain>, p);
   }
-  k_sieve<NG, MODE><<<grid, threads, smem, s>>>(p);
+  k_sieve<NG, MODE, kPlain><<<grid, threads, smem, s>>>(p);
   return cudaGetLastError();
+}
+
+template <int NG, int MODE>
+static cudaError_t launch_t(const SieveParams &p, int grid, int threads, size_t smem, cudaStream_t s) {
+  // primes with <= kPlainHits hits per segment exist: the plain-prime pass
+  // (instantiated for the default wheel only; other wheels keep the (C) loops)
+  if constexpr (NG == SIEVE_PLAIN_NG && MODE != kBatch && SIEVE_COUNT_PLAIN) {
+    if ((uint64_t)p.r > p.seg_bits / kPlainHits) return launch_tp<NG, MODE, true>(p, grid, threads, smem, s);
+  }
+  return launch_tp<NG, MODE, false>(p, grid, threads, smem, s);
 }
 
 template <int MODE>
@@ -2060,6 +2077,11 @@ template <int NG>
 static cudaError_t set_attr_ng(size_t smem) {
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(k_sieve<NG, kCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  if constexpr (NG == SIEVE_PLAIN_NG) {
+    if ((e = cudaFuncSetAttribute(k_sieve<NG, kCount, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = cudaFuncSetAttribute(k_sieve<NG, kBitmap, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = cudaFuncSetAttribute(k_sieve<NG, kList, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  }
   if ((e = cudaFuncSetAttribute(k_sieve<NG, kBitmap>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
   if ((e = cudaFuncSetAttribute(k_sieve<NG, kBatch>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
   return cudaFuncSetAttribute(k_sieve<NG, kList>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
