@@ -112,6 +112,10 @@ with open(os.path.join(DST, f"{tag}_ncu_sieve.txt"), "w") as f:
     f.write(f"atomic lane utilisation = {lane_atoms / (nsm * 32 * cycles):.3f} of 148 x 32 lanes x cycles\n")
     f.write(f"dram bytes per launch = {dram:.0f}\n")
     f.write("\n# launch list shares (ncu, cold-cache, serialised)\n")
+    step_ns = sum(ns for k, (n, ns) in tot.items() if "k_k0_atomics" not in k)
     for k, (n, ns) in sorted(tot.items(), key=lambda x: -x[1][1]):
-        f.write(f"{k}: launches={n} total_us={ns / 1e3:.1f} share={ns / all_ns:.3f}\n")
+        diag = "k_k0_atomics" in k
+        f.write(f"{k}: launches={n} total_us={ns / 1e3:.1f} share={ns / all_ns:.3f}"
+                + ("  (K0 microbenchmark, outside the timed steps)" if diag
+                   else f" share_without_K0={ns / step_ns:.3f}") + "\n")
 print(open(os.path.join(DST, f"{tag}_ncu_sieve.txt")).read())
