@@ -136,6 +136,9 @@ constexpr uint32_t kSmemAlign = 128;
 #ifndef SIEVE_TMA_STORE  // A7 bitmap write-back by cp.async.bulk (0: 128-bit st.global)
 #define SIEVE_TMA_STORE 1
 #endif
+#ifndef SIEVE_WHEEL_DIAG  // diagnostics builds only: 1 = wheel init without table-index updates (wrong results)
+#define SIEVE_WHEEL_DIAG 0
+#endif
 #ifndef SIEVE_WB_DIAG  // diagnostics builds only: 1 = no wait for the bulk copy's reads, 2 = no bulk copy, 3 = no transpose
 #define SIEVE_WB_DIAG 0
 #endif

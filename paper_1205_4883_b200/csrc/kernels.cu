@@ -181,8 +181,12 @@ __device__ __forceinline__ uint32_t wheel_word(const char *tabb, uint32_t (&ig)[
     return 0u;
   } else {
     const uint32_t v = *reinterpret_cast<const uint32_t *>(tabb + 4u * WheelGroup<G>::OFF + ig[G]);
+#if SIEVE_WHEEL_DIAG == 1  // diagnostics build only: no index update (wrong pattern, in bounds)
+    (void)d4; (void)e4;
+#else
     const uint32_t t = ig[G] - e4[G];
     ig[G] = min(ig[G] + d4[G], t);
+#endif
     return v | wheel_word<G + 1, NG>(tabb, ig, d4, e4);
   }
 }
