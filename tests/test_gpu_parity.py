@@ -504,3 +504,53 @@ def test_batch_async_device_plan():
         assert np.array_equal(got[0::2][keep], oc[keep]) and np.array_equal(got[1::2][keep], os_[keep])
     finally:
         sv.set_stream(None)
+
+
+@pytest.mark.parametrize("cfg", ["config3", "config4"])
+def test_full_size_bitmaps_sampled_windows(cfg):
+    """Bitmap mode at full size, in the launch configuration the bench modes
+    time (sieve_bitmap_base_async: base primes, sieve and write-back in one
+    launch, device output): config 3's 625 MB bitmap of [2, 10^10] and config
+    4's 625 MB bitmap of [10^12, 10^12 + 10^10).  Properties over the whole
+    bitmap (popcount = count minus the prime 2, padding bits zero) and 16
+    seeded word-aligned windows of 10^6 integers element-wise against the
+    oracle's bitmap of the same window (reading R5: word j of the call covers
+    the odd integers o0 + 64 j ... o0 + 64 j + 62)."""
+    torch = pytest.importorskip("torch")
+    from paper_1205_4883_b200 import dist as D
+    lo, hi = inputs.CONFIG3 if cfg == "config3" else inputs.CONFIG4
+    want = (int(PINS[f"{cfg}.count"]), int(PINS[f"{cfg}.sum"]))
+    r = D.isqrt(hi - 1)
+    base = D.alloc_base(sv.base_capacity(r), torch.device("cuda"))
+    words = sv.bitmap_words(lo, hi)
+    out = torch.empty(words, dtype=torch.int32, device="cuda")
+    res = torch.zeros(2, dtype=torch.int64, device="cuda")
+    sv.set_stream(torch.cuda.current_stream())
+    try:
+        sv.bitmap_base_async(lo, hi, base.primes, base.recips, base.nbase, out, res)
+        torch.cuda.synchronize()
+    finally:
+        sv.set_stream(None)
+    assert tuple(int(x) & MASK64 for x in res.cpu().tolist()) == want
+    x = out.to(torch.int64) & 0xFFFFFFFF  # SWAR popcount on the device
+    x = x - ((x >> 1) & 0x55555555)
+    x = (x & 0x33333333) + ((x >> 2) & 0x33333333)
+    x = (x + (x >> 4)) & 0x0F0F0F0F
+    pc = int(((x * 0x01010101) >> 24 & 0xFF).sum().item())
+    del x
+    w = out.cpu().numpy().view(np.uint32)
+    assert pc + (1 if lo <= 2 < hi else 0) == want[0]
+    B = hi // 2 - lo // 2
+    if B % 32:
+        assert int(w[-1]) >> (B % 32) == 0
+    o0 = lo | 1
+    g = inputs.SplitMix64(31 + len(cfg))
+    for _ in range(16):
+        w0 = g.next() % (words - 20000)
+        w1 = w0 + 15625  # 10^6 integers
+        a, b = o0 + 64 * w0, o0 + 64 * w1
+        obm, _, _ = oracle.bitmap(a, b)
+        assert obm.size == w1 - w0
+        assert np.array_equal(w[w0:w1], obm), (cfg, w0)
+    del out
+    torch.cuda.empty_cache()
