@@ -83,6 +83,23 @@ __device__ __forceinline__ uint32_t first_hit_above(uint64_t a, uint32_t p, uint
   return min(j, j - p);  // r = 0: j = p -> 0
 }
 
+// first_hit_above with one 32-bit multiply-high instead of the 64 x 64 one,
+// for a < 2^(32+t) and p > 2^t (t uniform, sh = 32 - t, a_sh = a >> t,
+// na_lo = -a mod 2^32): M = recip >> sh = floor(2^(32+t)/p) < 2^32 (recip =
+// floor(2^64/p) for odd p, and floors nest), q = hi32(a_sh M) is floor(a/p)
+// less 0, 1 or 2 (each truncation costs under one unit), so d = (q + 3) p - a
+// is -a mod p plus 0, p or 2 p, in (0, 3p] (p < 2^30: no wrap).  The odd
+// multiple a + 2 j' with 2 j' = d or d + p (whichever is even) has j' in
+// (0, 2p]; two conditional subtractions give j in [0, p).
+__device__ __forceinline__ uint32_t first_hit_scaled(uint32_t a_sh, uint32_t na_lo, uint32_t sh,
+                                                     uint32_t p, uint64_t recip) {
+  const uint32_t M = __funnelshift_rc((uint32_t)recip, (uint32_t)(recip >> 32), sh);
+  const uint32_t d = (__umulhi(a_sh, M) + 3u) * p + na_lo;
+  uint32_t j = (d + ((d & 1u) ? p : 0u)) >> 1;
+  j = min(j, j - p);
+  return min(j, j - p);
+}
+
 // floor((2^64-1)/p) for an odd p >= 3, without a 64-bit integer division:
 // a double quotient (within 2^12 of the result), then the exact remainder
 // T = (2^64-1) - q p (|T| < 2^40, so mod-2^64 arithmetic gives it as a signed
@@ -569,34 +586,60 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // item) for ~1.1e9 pairs, most of them without a hit.)
   if constexpr (kPlainTwo) {
     constexpr int U = kPlainU > 0 ? kPlainU : 1;
-    for (uint32_t k0 = two; k0 < c_end; k0 += U * blockDim.x) {
+    // a first hit of kFar puts the walk start past Jlim: no hit, no branch
+    constexpr uint32_t kFar = 1u << 29;
+    // the scale of first_hit_scaled: a < 2^(32+t), every plain prime > 2^t
+    // (the first is the smallest), t <= 28 so that p < 2^30
+    const uint32_t t = (a >> 32) ? 32u - __clz((uint32_t)(a >> 32)) : 0u;
+    const bool scaled = two < c_end && t <= 28u && (1u << t) < __ldg(primes + two);
+    const uint32_t a_sh = (uint32_t)(a >> t), na_lo = 0u - (uint32_t)a, sh = 32u - t;
+    // one pass of U primes per thread; kFull: all of them below c_end (no
+    // clamp, no compare).  Returns false when p^2 is past the segment.
+    auto plain_pass = [&](uint32_t k0, auto full) -> bool {
+      constexpr bool kFull = decltype(full)::value;
       uint32_t pk[U], jk[U], kk[U];
       uint64_t rk[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         kk[u] = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
-        const uint32_t k = min(kk[u], c_end - 1u);
+        const uint32_t k = kFull ? kk[u] : min(kk[u], c_end - 1u);
         pk[u] = __ldg(primes + k);
         rk[u] = __ldg(recips + k);
       }
       if ((uint64_t)pk[U - 1] * pk[U - 1] <= a) {  // the largest of the pass: so for all
+        if (scaled) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) jk[u] = kk[u] < c_end ? first_hit_above(a, pk[u], rk[u]) : kNone;
+          for (int u = 0; u < U; ++u) {
+            const uint32_t j = first_hit_scaled(a_sh, na_lo, sh, pk[u], rk[u]);
+            jk[u] = (kFull || kk[u] < c_end) ? j : kFar;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t j = first_hit_above(a, pk[u], rk[u]);
+            jk[u] = (kFull || kk[u] < c_end) ? j : kFar;
+          }
+        }
       } else {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
-          if (kk[u] >= c_end) jk[u] = kNone;
+          const uint32_t j = first_hit(a, seg_end, pk[u], rk[u]);
+          jk[u] = ((!kFull && kk[u] >= c_end) || j == kNone) ? kFar : j;
         }
-        if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
+        if (jk[0] == kFar) return false;  // p^2 past the segment: so for every later prime
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (jk[u] == kNone) break;  // past c_end (or p^2 past the segment), and so the later ones
         const uint32_t P4 = 4u * pk[u];
         for (uint32_t J = 4u * jk[u] + 32u * sb; J < Jlim; J += P4) red_or(j_addr(J), j_mask(J));
       }
-    }
+      return true;
+    };
+    const uint32_t step = U * blockDim.x;
+    uint32_t k0 = two;
+    bool more = true;
+    for (; more && c_end - k0 >= step && k0 < c_end; k0 += step) more = plain_pass(k0, std::true_type{});
+    if (more && k0 < c_end) plain_pass(k0, std::false_type{});
   }
   if (prof) {  // per-warp busy cycles of the regions (diagnostics only)
     const long long t4 = clock64();

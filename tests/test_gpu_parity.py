@@ -433,6 +433,28 @@ def test_batch_edge_intervals():
         assert (int(c[k]), int(s[k])) == oracle.stats(a, b), (a, b)
 
 
+@pytest.mark.parametrize("seg_kb", [16, 64, 208])
+def test_batch_plain_pass_magnitudes(seg_kb):
+    """The batch kernel's plain pass (primes with <= 8 hits per item) takes
+    the 32-bit scaled first hit when every such prime exceeds 2^t, a < 2^(32+t)
+    (default segment: everywhere below 2^48), else the 64-bit Barrett one
+    (16 KiB segments above ~2^46): random intervals from 2^20 to 2^48 over
+    both, with full and partial passes, vs the oracle."""
+    sv.set_options(segment_kb=seg_kb)
+    rng = np.random.default_rng(4242 + seg_kb)
+    iv = []
+    for e in range(20, 49, 2):
+        for _ in range(3):
+            b = int(rng.integers(1, 4 * 10**5))
+            a = int(rng.integers(1 << (e - 1), (1 << e) - b)) if e < 48 else (1 << 48) - b
+            iv.append((a, a + b))
+    lo = np.array([a for a, _ in iv], dtype=np.uint64)
+    hi = np.array([b for _, b in iv], dtype=np.uint64)
+    c, s = sv.batch(lo, hi)
+    for k, (a, b) in enumerate(iv):
+        assert (int(c[k]), int(s[k])) == oracle.stats(a, b), (seg_kb, a, b)
+
+
 @pytest.mark.parametrize("lo,hi", [(2, 48), (40, 43), (1, 3), (29, 32), (2, 10**6), (999_983, 10**6 + 7)])
 def test_small_ranges_fused_sync_paths(lo, hi):
     """Ranges around the wheel primes and tiny ranges through the synchronous

@@ -25,10 +25,13 @@ def _captured_kernel(report):
     out = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     name = rows[2][rows[0].index("Kernel Name")]
-    m = re.search(r"k_sieve<(\d+), (\d+)>", name)
+    m = re.search(r"k_sieve<(\d+), (\d+)(?:, (\d+|true|false))?>", name)
     if not m:
         raise SystemExit(f"not a k_sieve capture: {name}")
-    return f"_ZN2sv7k_sieveILi{m.group(1)}ELi{m.group(2)}EEEvNS_11SieveParamsE"
+    if m.group(3) is None:  # round-1 kernels: two template parameters
+        return f"_ZN2sv7k_sieveILi{m.group(1)}ELi{m.group(2)}EEEvNS_11SieveParamsE"
+    b = 1 if m.group(3) in ("1", "true") else 0
+    return f"_ZN2sv7k_sieveILi{m.group(1)}ELi{m.group(2)}ELb{b}EEEvNS_11SieveParamsE"
 
 
 fn = sys.argv[2] if len(sys.argv) > 2 else _captured_kernel(rep)
