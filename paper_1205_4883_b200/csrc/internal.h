@@ -82,6 +82,11 @@ constexpr uint32_t kWarpHits = SIEVE_WARP_HITS;
 #define SIEVE_C15_HITS 32  // A/B: 16, 32, 48 -> 32
 #endif
 constexpr uint32_t kC15Hits = SIEVE_C15_HITS;
+// (C) first hits by first_hit_scaled where the lane's largest prime has
+// p^2 <= a (else first_hit with the p^2 clamp)
+#ifndef SIEVE_C_SCALED
+#define SIEVE_C_SCALED 1
+#endif
 // batch kernel: (C) primes with at most kPlainHits hits per segment are
 // marked without the multiple-of-3 skip
 #ifndef SIEVE_PLAIN_HITS

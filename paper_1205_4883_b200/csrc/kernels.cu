@@ -514,6 +514,21 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
   // multiples of 5 as well (8 kept hits per period of 15); [few, c_end) skip
   // the multiples of 3 only.  Two loops: no per-lane branch on the walk kind.
   const uint32_t few = min(R.few, c_end);
+  // the scale of first_hit_scaled: a < 2^(32+t); the walks use it when every
+  // prime of the region exceeds 2^t (the region's first prime is its
+  // smallest) and t <= 28 (p < 2^30).  Only in the kernels with the plain
+  // pass (r > S / kPlainHits): there the (C) walks gain too (configs 4 and 5:
+  // 1.7 % / 1.4 %), while in the others config 3 (+0.5 %) and config 2
+  // (+1.5 %) lose (profiles/r02_negative_ab.txt item 12).
+  uint32_t t = 0, a_sh = 0, na_lo = 0, sh = 32;
+  bool scaled_c = false;
+  if constexpr (kPlainTwo) {
+    t = (a >> 32) ? 32u - __clz((uint32_t)(a >> 32)) : 0u;
+    a_sh = (uint32_t)(a >> t);
+    na_lo = 0u - (uint32_t)a;
+    sh = 32u - t;
+    scaled_c = SIEVE_C_SCALED && R.warp < c_end && t <= 28u && (1u << t) < __ldg(primes + R.warp);
+  }
   auto c_loop = [&](uint32_t cb, uint32_t ce, auto by15) {
     for (uint32_t k0 = cb; k0 < ce; k0 += kLargeILP * blockDim.x) {
       uint32_t pk[kLargeILP], jk[kLargeILP];
@@ -525,11 +540,20 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
         pk[u] = __ldg(primes + k);
         rk[u] = __ldg(recips + k);
       }
+      if (kPlainTwo && scaled_c && (uint64_t)pk[kLargeILP - 1] * pk[kLargeILP - 1] <= a) {  // the lane's largest
 #pragma unroll
-      for (int u = 0; u < kLargeILP; ++u) {
-        jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
-        const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
-        if (ku >= ce) jk[u] = kNone;
+        for (int u = 0; u < kLargeILP; ++u) {
+          const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+          const uint32_t j = first_hit_scaled(a_sh, na_lo, sh, pk[u], rk[u]);
+          jk[u] = ku >= ce ? kNone : j;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kLargeILP; ++u) {
+          jk[u] = first_hit(a, seg_end, pk[u], rk[u]);
+          const uint32_t ku = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+          if (ku >= ce) jk[u] = kNone;
+        }
       }
       if (jk[0] == kNone) break;  // p^2 past the segment: so for every later prime
 #pragma unroll
@@ -588,11 +612,8 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
     constexpr int U = kPlainU > 0 ? kPlainU : 1;
     // a first hit of kFar puts the walk start past Jlim: no hit, no branch
     constexpr uint32_t kFar = 1u << 29;
-    // the scale of first_hit_scaled: a < 2^(32+t), every plain prime > 2^t
-    // (the first is the smallest), t <= 28 so that p < 2^30
-    const uint32_t t = (a >> 32) ? 32u - __clz((uint32_t)(a >> 32)) : 0u;
+    // first_hit_scaled when every plain prime > 2^t (the first is the smallest)
     const bool scaled = two < c_end && t <= 28u && (1u << t) < __ldg(primes + two);
-    const uint32_t a_sh = (uint32_t)(a >> t), na_lo = 0u - (uint32_t)a, sh = 32u - t;
     // one pass of U primes per thread; kFull: all of them below c_end (no
     // clamp, no compare).  Returns false when p^2 is past the segment.
     auto plain_pass = [&](uint32_t k0, auto full) -> bool {
