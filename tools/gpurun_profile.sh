@@ -1,6 +1,7 @@
 # Round profiling pass (run under gpurun): GPU tests, bench, modes + oracle
 # report, K0, per-rank blocks, F3 A/B, phase counters, the ncu launch list and
-# one `--set full` capture of the sieve kernel.
+# `--set full` captures of the sieve kernel (config 3 from bench.py, the
+# config-5 batch kernel, the config-4 count kernel).
 # tools/make_profile_summary.py <tag> turns gpurun_out/ into profiles/.
 set -x
 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -5 gpurun_out/pytest_gpu.log
@@ -12,4 +13,6 @@ python tools/f3_ab.py > gpurun_out/f3_ab.jsonl 2>&1; cat gpurun_out/f3_ab.jsonl
 python tools/phase_prof.py > gpurun_out/phase.json 2>&1
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
 python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/plain2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_sieve -c 1 -o gpurun_out/prof_sieve python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+python tools/one_batch.py > gpurun_out/ob.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_sieve -c 1 -o gpurun_out/prof_batch python tools/one_batch.py > gpurun_out/ncu_batch.log 2>&1
+RANGE=1000000000000,1010000000000 python tools/one_launch.py > gpurun_out/ol.log 2>&1 && RANGE=1000000000000,1010000000000 ncu --set full --clock-control none --import-source on -k regex:k_sieve -c 1 -o gpurun_out/prof_config4 python tools/one_launch.py > gpurun_out/ncu_c4.log 2>&1
 ls -la gpurun_out

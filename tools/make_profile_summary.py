@@ -6,6 +6,7 @@ into the committed evidence under profiles/:
   profiles/<tag>_k0_peaks.json       shared-memory / HBM microbenchmarks
   profiles/<tag>_launches.csv        ncu launch list (gpu__time_duration.sum)
   profiles/<tag>_ncu_sieve.txt       key counters of one `ncu --set full` capture
+  profiles/<tag>_ncu_*regions.txt    per-region breakdowns (config 3, 5, 4 captures)
   profiles/ncu_sieve_summary.json    per-launch DRAM traffic of the sieve kernel
                                      (read by bench.py for roofline.traffic)
 """
@@ -119,3 +120,15 @@ with open(os.path.join(DST, f"{tag}_ncu_sieve.txt"), "w") as f:
                 + ("  (K0 microbenchmark, outside the timed steps)" if diag
                    else f" share_without_K0={ns / step_ns:.3f}") + "\n")
 print(open(os.path.join(DST, f"{tag}_ncu_sieve.txt")).read())
+
+# per-region breakdowns (tools/sass_regions.py) of the captures present
+for cap, name, what in [("prof_sieve.ncu-rep", "ncu_regions", "config 3, bench.py step"),
+                        ("prof_batch.ncu-rep", "ncu_batch_regions", "config 5, sieve_batch_async"),
+                        ("prof_config4.ncu-rep", "ncu_config4_regions", "config 4, count kernel")]:
+    cp = os.path.join(SRC, cap)
+    if os.path.exists(cp):
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_regions.py"), cp],
+                             capture_output=True, text=True).stdout
+        with open(os.path.join(DST, f"{tag}_{name}.txt"), "w") as f:
+            f.write(f"# tools/sass_regions.py on the ncu --set full capture of {what} ({tag})\n{out}")
+        print(out)

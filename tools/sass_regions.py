@@ -1,7 +1,7 @@
 """Per-region cost breakdown of the sieve kernel from one `ncu --set full`
 capture: instructions by pipe class, shared-memory wavefronts (actual and
 ideal) and warp-stall samples, attributed to the marking regions (A1, A2, B,
-C), the wheel init, the epilogue and the rest, through the inlined-line
+C; the plain pass of the batch / kPlain kernels), the wheel init, the epilogue and the rest, through the inlined-line
 annotations of `nvdisasm -gi` (the library is built with -lineinfo).
 
 Usage: python tools/sass_regions.py REPORT [KERNEL_MANGLED]
@@ -53,7 +53,8 @@ regions = [
     ("A1", line_of(r"// \(A1\) units", ms), line_of(r"// \(A2\) ", ms)),
     ("A2", line_of(r"// \(A2\) ", ms), line_of(r"// \(B\) one prime per warp", ms)),
     ("B", line_of(r"// \(B\) one prime per warp", ms), line_of(r"// \(C\) large primes", ms)),
-    ("C", line_of(r"// \(C\) large primes", ms), line_of(r"^// In-place 32x32|^// -+\n// A5|^__device__ __forceinline__ uint2 \*bucket_at", ms)),
+    ("C", line_of(r"// \(C\) large primes", ms), line_of(r"// The plain primes \(batch kernel\)", ms)),
+    ("plain", line_of(r"// The plain primes \(batch kernel\)", ms), line_of(r"if \(prof\) \{  // per-warp busy cycles", ms)),
     ("bucket", line_of(r"^__device__ __forceinline__ uint2 \*bucket_at"), line_of(r"^// In-place 32x32")),
     ("untranspose", line_of(r"^// In-place 32x32"), line_of(r"^// A6/A7: count, sum")),
     ("epilogue", line_of(r"^// A6/A7: count, sum"), line_of(r"^// block-wide sum of two u64")),
