@@ -95,7 +95,9 @@ __device__ __forceinline__ uint32_t first_hit_scaled(uint32_t a_sh, uint32_t na_
                                                      uint32_t p, uint64_t recip) {
   const uint32_t M = __funnelshift_rc((uint32_t)recip, (uint32_t)(recip >> 32), sh);
   const uint32_t d = (__umulhi(a_sh, M) + 3u) * p + na_lo;
-  uint32_t j = (d + ((d & 1u) ? p : 0u)) >> 1;
+  uint32_t j2;  // d + (d & 1) p as one lop3 + one imad (a select costs two more)
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(j2) : "r"(d & 1u), "r"(p), "r"(d));
+  uint32_t j = j2 >> 1;
   j = min(j, j - p);
   return min(j, j - p);
 }

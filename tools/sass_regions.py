@@ -136,7 +136,7 @@ for r in data:
 tot = {k: sum(a[k] for a in agg.values()) for k in ("inst", "wf", "samp")}
 print(f"{'region':12s} {'samp%':>6s} {'inst M':>8s} {'alu M':>7s} {'fma M':>7s} {'lsu M':>7s} "
       f"{'atoms M':>8s} {'wf M':>7s} {'wf/ideal':>8s}")
-for reg in ["wheel", "A1", "A2", "B", "C", "bucket", "untranspose", "epilogue", "other"]:
+for reg in ["wheel", "A1", "A2", "B", "C", "plain", "bucket", "untranspose", "epilogue", "other"]:
     a = agg.get(reg)
     if not a:
         continue
@@ -144,3 +144,11 @@ for reg in ["wheel", "A1", "A2", "B", "C", "bucket", "untranspose", "epilogue", 
           f"{a['fma'] / 1e6:7.1f} {a['lsu'] / 1e6:7.1f} {a['atoms'] / 1e6:8.1f} {a['wf'] / 1e6:7.1f} "
           f"{(a['wf'] / a['wfi'] if a['wfi'] else 0):8.2f}")
 print(f"{'total':12s} {100.0:6.1f} {tot['inst'] / 1e6:8.1f} {'':7s} {'':7s} {'':7s} {'':8s} {tot['wf'] / 1e6:7.1f}")
+
+# SASS_DUMP=<region>: the region's instructions with their counts and samples
+if os.environ.get("SASS_DUMP"):
+    print(f"\n# {os.environ['SASS_DUMP']}: offset, executed (M warp instr), stall samples, SASS")
+    for r in data:
+        off = int(r[0], 16) - base
+        if off2reg.get(off, "other") == os.environ["SASS_DUMP"]:
+            print(f"{off:6x} {f(r, 'Instructions Executed') / 1e6:8.2f} {f(r, 'Warp Stall Sampling (All Samples)'):7.0f}  {r[1].strip()[:90]}")
