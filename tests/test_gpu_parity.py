@@ -6,6 +6,8 @@ finishes in seconds while spanning several segments and a ragged tail; the
 full BASELINE configs are checked against pinned values (tests/golden/) and
 on oracle-computable samples.
 """
+import math
+
 import numpy as np
 import pytest
 
@@ -453,6 +455,38 @@ def test_batch_plain_pass_magnitudes(seg_kb):
     c, s = sv.batch(lo, hi)
     for k, (a, b) in enumerate(iv):
         assert (int(c[k]), int(s[k])) == oracle.stats(a, b), (seg_kb, a, b)
+
+
+@pytest.mark.parametrize("shift", [0, 1, 2, 3])
+def test_plain_pass_list_alignment(shift):
+    """Caller-owned base-prime buffers at any 4-byte offset (views shifted
+    by 0-3 primes) through the base-buffer calls of the plain-pass kernels
+    (r > S/8): count, sum and the bitmap of a 3*10^7 window at 10^12
+    (r ~ 10^6) against the oracle."""
+    torch = pytest.importorskip("torch")
+    lo, hi = 10**12 + 17, 10**12 + 3 * 10**7 + 5
+    r = int(np.sqrt(hi)) + 1
+    cap = sv.base_capacity(r) + 4
+    dev = torch.device("cuda")
+    pbuf = torch.zeros(cap + 4, dtype=torch.int32, device=dev)
+    rbuf = torch.zeros(cap + 4, dtype=torch.int64, device=dev)
+    nb = torch.zeros(1, dtype=torch.int32, device=dev)
+    primes, recips = pbuf[shift: shift + cap], rbuf[shift: shift + cap]
+    res = torch.zeros(2, dtype=torch.int64, device=dev)
+    out = torch.empty(sv.bitmap_words(lo, hi), dtype=torch.int32, device=dev)
+    sv.set_stream(torch.cuda.current_stream())
+    try:
+        sv.base_primes_async(math.isqrt(hi - 1), primes, recips, nb)
+        sv.stats_async(lo, hi, primes, recips, nb, res)
+        torch.cuda.synchronize()
+        got = tuple(int(x) & MASK64 for x in res.cpu().tolist())
+        sv.bitmap_base_async(lo, hi, primes, recips, nb, out, res)
+        torch.cuda.synchronize()
+    finally:
+        sv.set_stream(None)
+    assert got == oracle.stats(lo, hi)
+    obm, _, _ = oracle.bitmap(lo, hi)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), obm)
 
 
 @pytest.mark.parametrize("lo,hi", [(2, 48), (40, 43), (1, 3), (29, 32), (2, 10**6), (999_983, 10**6 + 7)])
