@@ -57,7 +57,8 @@ regions = [
     ("plain", line_of(r"// The plain primes \(batch kernel\)", ms), line_of(r"if \(prof\) \{  // per-warp busy cycles", ms)),
     ("bucket", line_of(r"^__device__ __forceinline__ uint2 \*bucket_at"), line_of(r"^// In-place 32x32")),
     ("untranspose", line_of(r"^// In-place 32x32"), line_of(r"^// A6/A7: count, sum")),
-    ("epilogue", line_of(r"^// A6/A7: count, sum"), line_of(r"^// block-wide sum of two u64")),
+    ("epilogue", line_of(r"^// A6/A7: count, sum"), line_of(r"^constexpr uint64_t kFlagAgg")),
+    ("list", line_of(r"^constexpr uint64_t kFlagAgg"), line_of(r"^// block-wide sum of two u64")),
 ]
 
 
@@ -136,7 +137,7 @@ for r in data:
 tot = {k: sum(a[k] for a in agg.values()) for k in ("inst", "wf", "samp")}
 print(f"{'region':12s} {'samp%':>6s} {'inst M':>8s} {'alu M':>7s} {'fma M':>7s} {'lsu M':>7s} "
       f"{'atoms M':>8s} {'wf M':>7s} {'wf/ideal':>8s}")
-for reg in ["wheel", "A1", "A2", "B", "C", "plain", "bucket", "untranspose", "epilogue", "other"]:
+for reg in ["wheel", "A1", "A2", "B", "C", "plain", "bucket", "untranspose", "epilogue", "list", "other"]:
     a = agg.get(reg)
     if not a:
         continue
