@@ -69,7 +69,11 @@ typedef struct sieve_options {
                              1 = per-segment buckets (a skipped segment costs the prime nothing;
                              not used by sieve_batch, nor for ranges of more than 2^31 odd slots
                              per CTA, where the Barrett path runs) */
-    uint32_t reserved[3]; /* must be zero */
+    uint32_t bitmap_count_only; /* 1: sieve_bitmap_async / sieve_bitmap_base_async compute the count
+                             only and write result[1] = 0 (the write-back then needs no per-word
+                             POPC); 0 (default): result[1] = the prime sum.  sieve_bitmap, which
+                             returns the count alone, never computes the sum */
+    uint32_t reserved[2]; /* must be zero */
 } sieve_options;
 
 /* ---------------------------------------------------------------------- */

@@ -34,7 +34,8 @@ class SieveError(RuntimeError):
 class _Options(ctypes.Structure):
     _fields_ = [("segment_kb", ctypes.c_uint32), ("wheel", ctypes.c_uint32),
                 ("ctas_per_sm", ctypes.c_uint32), ("threads", ctypes.c_uint32),
-                ("buckets", ctypes.c_uint32), ("reserved", ctypes.c_uint32 * 3)]
+                ("buckets", ctypes.c_uint32), ("bitmap_count_only", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32 * 2)]
 
 
 _lib = None
@@ -337,8 +338,8 @@ def get_stream() -> int:
 
 
 def set_options(segment_kb: int = 0, wheel: int = 0, ctas_per_sm: int = 0, threads: int = 0,
-                buckets: int = 0) -> None:
-    o = _Options(segment_kb, wheel, ctas_per_sm, threads, buckets)
+                buckets: int = 0, bitmap_count_only: int = 0) -> None:
+    o = _Options(segment_kb, wheel, ctas_per_sm, threads, buckets, bitmap_count_only)
     _check(lib().sieve_set_options(ctypes.byref(o)))
 
 
@@ -346,7 +347,7 @@ def get_options() -> dict:
     o = _Options()
     _check(lib().sieve_get_options(ctypes.byref(o)))
     return {"segment_kb": o.segment_kb, "wheel": o.wheel, "ctas_per_sm": o.ctas_per_sm,
-            "threads": o.threads, "buckets": o.buckets}
+            "threads": o.threads, "buckets": o.buckets, "bitmap_count_only": o.bitmap_count_only}
 
 
 def shutdown() -> None:

@@ -150,6 +150,18 @@ constexpr uint32_t kSmemAlign = 128;
 #ifndef SIEVE_UNTRANSPOSE_ILP  // blocks per warp and pass of the bit transpose
 #define SIEVE_UNTRANSPOSE_ILP 2
 #endif
+#ifndef SIEVE_WB_FUSED  // bitmap mode: fused in-register transpose + count (writeback_fused)
+#define SIEVE_WB_FUSED 1
+#endif
+#ifndef SIEVE_WB_WARP_COPY  // fused write-back: one bulk copy per warp run (1) or per segment (0)
+#define SIEVE_WB_WARP_COPY 1
+#endif
+#ifndef SIEVE_WB_LANES  // lanes per 1024-slot block in the in-register transpose (2 or 4)
+#define SIEVE_WB_LANES 2
+#endif
+#ifndef SIEVE_REG_TRANSPOSE  // list mode: in-register transpose (1) or the shuffle transpose (0)
+#define SIEVE_REG_TRANSPOSE 1
+#endif
 #ifndef SIEVE_WHEEL_UNROLL  // unroll of the wheel-init word loop (count mode)
 #define SIEVE_WHEEL_UNROLL 4
 #endif
@@ -254,6 +266,10 @@ constexpr uint32_t kFlagNoCoop = 32u;
 // (two CTAs per super-segment, region C over distributed shared memory), base
 // primes by K1.  An A/B variant, not the product path.
 constexpr uint32_t kFlagCluster = 64u;
+// Bitmap mode without the prime sum (sieve_bitmap, option bitmap_count_only):
+// the write-back counts from carry-save planes only; result[1] = 0.  A
+// product flag, set by the runtime -- not a diagnostic.
+constexpr uint32_t kFlagNoSum = 128u;
 
 enum Mode { kCount = 0, kBitmap = 1, kBatch = 2, kList = 3 };
 

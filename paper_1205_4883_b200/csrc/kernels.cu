@@ -1005,6 +1005,281 @@ __device__ __forceinline__ void epilogue(const uint32_t *seg, uint64_t a, uint64
 #endif
 }
 
+// ---------------------------------------------------------------------------
+// Partial-block 32x32 bit transpose in registers (round 2 of A7; replaces
+// the shuffle transpose above in bitmap and list modes).  kWbLanes = L
+// lanes (u = lane mod L) share a 1024-slot block B: lane u holds rows
+// R u .. R u + R - 1 (R = 32 / L) of its 32 transposed words in R
+// registers.  Stage j (16, 8, 4, 2, 1) swaps the off-diagonal j x j
+// sub-blocks of every 2j x 2j block between the row pairs (r, r + j): the
+// lower row keeps its columns c with (c & j) == 0 and takes its partner's
+// low columns moved up by j, the upper row keeps its high columns and takes
+// its partner's high columns moved down -- a shift and a bit-select LOP3 per
+// row.  Stages j >= R pair two lanes (one SHFL per row: with L = 4, stages
+// 16 and 8); the others pair registers of one lane.  The shuffle transpose
+// does all five stages with a SHFL per row (tools/transpose_bench.cu).
+// L = 4 (default) gives 4 x 1664 quarter blocks per 208 KiB segment, 6.5
+// per thread of 1024 -- 7 rounds, where halves take 4 rounds for 3.25 (the
+// slowest thread sets the phase; same-box A/B in DESIGN.md).
+//
+// Bank skew: a warp holds 32 / L consecutive blocks, 128 bytes apart, so
+// quad q of every block sits in the same 4 banks.  Lane (B, u) with
+// t = B mod (8 / L) therefore loads and stores quad (8 / L) u + (q ^ t) in
+// its q-th access (8 distinct quads over the warp: conflict-free LDS.128 /
+// STS.128).  Register i of the lane then holds row R u + (i ^ 4t), and
+// natural word R u + c must end in register c ^ 4t; the transpose absorbs
+// both XOR permutations (of the row and column index bits that 4t can set,
+// all below R): in those in-register stages j where bit j of 4t is set, the
+// pair's roles swap (the lower row keeps its high columns and takes the
+// partner's shifted down, and vice versa) -- a lane-dependent rotation
+// amount and mask, the same two instructions.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kWbLanes = SIEVE_WB_LANES;
+constexpr uint32_t kWbRows = 32u / kWbLanes;   // rows per lane
+constexpr uint32_t kWbQuads = kWbRows / 4u;    // quads per lane
+static_assert(kWbLanes == 2 || kWbLanes == 4, "SIEVE_WB_LANES is 2 or 4");
+
+__device__ __forceinline__ uint32_t bitsel(uint32_t x, uint32_t y, uint32_t k) {  // (x & k) | (y & ~k)
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(x), "r"(y), "r"(k));
+  return r;
+}
+template <uint32_t J>
+struct TMask {  // columns c with (c & J) == 0
+  static constexpr uint32_t v =
+      J == 16 ? 0x0000FFFFu : J == 8 ? 0x00FF00FFu : J == 4 ? 0x0F0F0F0Fu : J == 2 ? 0x33333333u : 0x55555555u;
+};
+// in-register stage, roles swapped where `flip`
+template <uint32_t J>
+__device__ __forceinline__ void tstage_reg(uint32_t (&A)[kWbRows], bool flip) {
+  if constexpr (J < kWbRows) {
+    constexpr uint32_t m = TMask<J>::v;
+    if (J >= 4) {  // lane-dependent (the skew reaches index bits 2 .. log2(kWbQuads) + 1)
+      const uint32_t keep = flip ? ~m : m, amt = flip ? 32u - J : J;
+#pragma unroll
+      for (int r = 0; r < (int)kWbRows; ++r) {
+        if (r & J) continue;
+        const uint32_t x = A[r], y = A[r + J];
+        A[r] = bitsel(x, __funnelshift_l(y, y, amt), keep);
+        A[r + J] = bitsel(__funnelshift_r(x, x, amt), y, keep);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < (int)kWbRows; ++r) {
+        if (r & J) continue;
+        const uint32_t x = A[r], y = A[r + J];
+        A[r] = bitsel(x, y << J, m);
+        A[r + J] = bitsel(x >> J, y, m);
+      }
+    }
+  }
+}
+// cross-lane stage j >= kWbRows: the partner is lane ^ (j / kWbRows); the
+// lower lane takes the partner's row rotated left by j, the upper lane the
+// partner's rotated right by j, so each lane sends its own row rotated the
+// way its partner needs
+template <uint32_t J>
+__device__ __forceinline__ void tstage_lane(uint32_t (&A)[kWbRows], uint32_t u) {
+  if constexpr (J >= kWbRows) {
+    constexpr uint32_t m = TMask<J>::v, x = J / kWbRows;
+    const bool upper = u & x;
+    const uint32_t keep = upper ? ~m : m, send = upper ? J : 32u - J;
+#pragma unroll
+    for (int r = 0; r < (int)kWbRows; ++r) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, __funnelshift_l(A[r], A[r], send), x);
+      A[r] = bitsel(A[r], y, keep);
+    }
+  }
+}
+// byte address (shared window) of the lane's first quad: its q-th quad is
+// qa ^ (16 q) (a block is 128-byte aligned, the lane's quads 16 kWbQuads)
+__device__ __forceinline__ uint32_t part_block_addr(const uint32_t *seg, uint32_t B, uint32_t u) {
+  return (uint32_t)__cvta_generic_to_shared(seg) + 128u * B + 16u * kWbQuads * u + 16u * (B & (kWbQuads - 1u));
+}
+__device__ __forceinline__ void load_part_block(uint32_t qa, uint32_t (&A)[kWbRows]) {
+#pragma unroll
+  for (int q = 0; q < (int)kWbQuads; ++q)
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(A[4 * q]), "=r"(A[4 * q + 1]), "=r"(A[4 * q + 2]), "=r"(A[4 * q + 3])
+                 : "r"(qa ^ (16u * q)));
+}
+template <bool kInvert>
+__device__ __forceinline__ void store_part_block(uint32_t qa, const uint32_t (&A)[kWbRows]) {
+  SV_CHECK((qa | (16u * (kWbQuads - 1u))) + 16u <= s_chk_hi, kVioScratch);
+#pragma unroll
+  for (int q = 0; q < (int)kWbQuads; ++q) {
+    if (kInvert)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(qa ^ (16u * q)), "r"(~A[4 * q]),
+                   "r"(~A[4 * q + 1]), "r"(~A[4 * q + 2]), "r"(~A[4 * q + 3]) : "memory");
+    else
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(qa ^ (16u * q)), "r"(A[4 * q]),
+                   "r"(A[4 * q + 1]), "r"(A[4 * q + 2]), "r"(A[4 * q + 3]) : "memory");
+  }
+}
+// rows -> natural words of the lane's part (register c = natural word
+// kWbRows u + (c ^ 4t)).  Every lane of the warp must call it (shuffles).
+__device__ __forceinline__ void transpose_part_block(uint32_t B, uint32_t u, uint32_t (&A)[kWbRows]) {
+  tstage_lane<16>(A, u);
+  tstage_lane<8>(A, u);
+  const uint32_t k = 4u * (B & (kWbQuads - 1u));
+  tstage_reg<8>(A, k & 8u);
+  tstage_reg<4>(A, k & 4u);
+  tstage_reg<2>(A, false);
+  tstage_reg<1>(A, false);
+}
+
+// list mode: the in-place transpose of every block (no inversion)
+__device__ __forceinline__ void untranspose_reg(uint32_t *seg, uint32_t valid) {
+  const uint32_t nblk = (valid + 1023u) >> 10, lane = threadIdx.x & 31u, u = lane & (kWbLanes - 1u);
+  for (uint32_t P0 = threadIdx.x & ~31u; P0 < kWbLanes * nblk; P0 += blockDim.x) {
+    const bool own = (P0 + lane) / kWbLanes < nblk;
+    const uint32_t B = min((P0 + lane) / kWbLanes, nblk - 1u);  // tail lanes redo the last block
+    const uint32_t qa = part_block_addr(seg, B, u);
+    uint32_t A[kWbRows];
+    load_part_block(qa, A);
+    transpose_part_block(B, u, A);
+    __syncwarp();  // every lane's loads before a duplicate of the last block is stored
+    if (own) store_part_block<false>(qa, A);
+  }
+}
+
+// Carry-save accumulation of a lane's kWbRows prime words into 8 bit-sliced
+// planes (plane k = bit k of the per-bit-position count, counts < 256),
+// depth first: one CSA (two LOP3) per word and a short ripple of the top
+// carry -- the count for a few ALU instructions per word and no POPC (POPC
+// issues at a quarter of the LOP3 rate, tools/pipe_bench.cu: 0.5 vs 2 warp
+// instructions per clock and SM).
+__device__ __forceinline__ void planes_add(uint32_t (&pl)[8], const uint32_t (&A)[kWbRows]) {
+  uint32_t c8[kWbRows / 8];
+#pragma unroll
+  for (int g = 0; g < (int)kWbRows / 8; ++g) {
+    const uint32_t *w = A + 8 * g;
+    uint32_t a, b, fA, fB;
+    csa(a, pl[0], pl[0], ~w[0], ~w[1]);
+    csa(b, pl[0], pl[0], ~w[2], ~w[3]);
+    csa(fA, pl[1], pl[1], a, b);
+    csa(a, pl[0], pl[0], ~w[4], ~w[5]);
+    csa(b, pl[0], pl[0], ~w[6], ~w[7]);
+    csa(fB, pl[1], pl[1], a, b);
+    csa(c8[g], pl[2], pl[2], fA, fB);
+  }
+  uint32_t cy;
+  int k = 3;
+  if constexpr (kWbRows == 16) {
+    csa(cy, pl[3], pl[3], c8[0], c8[1]);
+    k = 4;
+  } else {
+    cy = c8[0];
+  }
+#pragma unroll
+  for (; k < 8; ++k) {
+    const uint32_t t = pl[k] & cy;
+    pl[k] ^= cy;
+    cy = t;
+  }
+}
+
+// A6/A7 fused (bitmap mode): per part block, count and sum from the
+// transposed rows as loaded, then transpose in registers, invert to prime
+// words and store them back (natural layout) -- no second pass over the
+// segment.  Input row b (bit n) of block B is natural word n (bit b), slot
+// 1024 B + 32 n + b, so over the prime bits
+//   sum of slots = 1024 sum_B B C_B + 32 sum_n n c_n + sum_b b r_b
+// with r_b = 32 - popc(row b) (a POPC per row, also giving C_B) and c_n =
+// 32 - popc(natural word n) (a POPC per transposed word), each lane adding
+// its part.  The words go to HBM by TMA bulk copies (cp.async.bulk): with
+// SIEVE_WB_WARP_COPY each warp sends its 32 / L consecutive blocks as soon
+// as its lanes have stored them, so the copies drain while the other warps
+// transpose; otherwise one copy per segment after a block barrier.  Words
+// past the 16-byte bulk prefix (and every word of an output that is not
+// 16-byte aligned) are stored from shared memory after a barrier.
+// kSum = false (kFlagNoSum: sieve_bitmap, option bitmap_count_only): the
+// count alone, from carry-save planes of the prime words (no POPC per word).
+template <bool kSum>
+__device__ __forceinline__ void writeback_fused(uint32_t *seg, uint64_t a, uint64_t bit0, uint32_t valid,
+                                                uint32_t *out, uint64_t out_words, uint32_t vec4,
+                                                unsigned long long &cnt, unsigned long long &sum) {
+  const uint32_t nblk = (valid + 1023u) >> 10;
+  const uint32_t lane = threadIdx.x & 31u, u = lane & (kWbLanes - 1u);
+  const uint64_t w0 = bit0 >> 5;
+  const uint32_t nq = (valid + 127u) >> 7;
+  const uint32_t nw = out_words > w0 ? (uint32_t)min((uint64_t)4u * nq, out_words - w0) : 0u;
+  const uint32_t n16 = (SIEVE_TMA_STORE && vec4) ? (nw & ~3u) : 0u;
+  // composite bits, sum of (row) x popc(row), sum of (word) x popc(word), sum of B x (prime bits)
+  uint32_t comp = 0, wrow = 0, wnat = 0, bc = 0, np = 0;
+  uint32_t pl[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // kSum = false: planes of the prime words
+  for (uint32_t P0 = threadIdx.x & ~31u; P0 < kWbLanes * nblk; P0 += blockDim.x) {
+    const bool own = (P0 + lane) / kWbLanes < nblk;
+    const uint32_t B = min((P0 + lane) / kWbLanes, nblk - 1u);  // tail lanes redo the last block, uncounted
+    const uint32_t qa = part_block_addr(seg, B, u);
+    const uint32_t t4 = 4u * (B & (kWbQuads - 1u)) + kWbRows * u;  // index of register 4q + e: (t4 ^ 4q) + e
+    uint32_t A[kWbRows];
+    load_part_block(qa, A);
+    uint32_t cb = 0, wr = 0;
+#pragma unroll
+    for (int q = 0; q < (int)kWbQuads && kSum; ++q) {  // register 4q + e = row (t4 ^ 4q) + e
+      const uint32_t c0 = __popc(A[4 * q]), c1 = __popc(A[4 * q + 1]), c2 = __popc(A[4 * q + 2]),
+                     c3 = __popc(A[4 * q + 3]);
+      const uint32_t cq = c0 + c1 + c2 + c3;
+      cb += cq;
+      wr += (t4 ^ (4u * q)) * cq + c1 + 2u * c2 + 3u * c3;
+    }
+    if (SIEVE_WB_DIAG != 3) transpose_part_block(B, u, A);
+    uint32_t wn = 0;
+#pragma unroll
+    for (int q = 0; q < (int)kWbQuads && kSum; ++q) {  // register 4q + e = natural word (t4 ^ 4q) + e
+      const uint32_t c1 = __popc(A[4 * q + 1]), c2 = __popc(A[4 * q + 2]), c3 = __popc(A[4 * q + 3]);
+      wn += (t4 ^ (4u * q)) * (__popc(A[4 * q]) + c1 + c2 + c3) + c1 + 2u * c2 + 3u * c3;
+    }
+    if (!kSum && own) planes_add(pl, A);
+    if (kSum && own) {
+      comp += cb;
+      wrow += wr;
+      wnat += wn;
+      bc += B * (32u * kWbRows - cb);
+      ++np;
+    }
+    __syncwarp();  // every lane's loads before a duplicate of the last block is stored
+    if (own) store_part_block<true>(qa, A);
+#if SIEVE_WB_WARP_COPY
+    const uint32_t wa = 32u * (P0 / kWbLanes);  // first word of the warp's blocks
+    if (n16 > wa) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && SIEVE_WB_DIAG != 2)
+        bulk_store(out + w0 + wa, seg + wa, 4u * min(32u * 32u / kWbLanes, n16 - wa));
+    }
+#endif
+  }
+#if !SIEVE_WB_WARP_COPY
+  if (n16) fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0 && n16 && SIEVE_WB_DIAG != 2) bulk_store(out + w0, seg, 4u * n16);
+#else
+  if (n16 < nw) __syncthreads();
+#endif
+  for (uint32_t w = n16 + threadIdx.x; w < nw; w += blockDim.x) {
+    SV_CHECK(w0 + w < out_words, kVioBitmapStore);
+    out[w0 + w] = seg[w];
+  }
+  if (kSum) {
+    // per part: kWbRows rows / words of 32 bits with indices R u .. R u + R - 1
+    const uint32_t C = 32u * kWbRows * np - comp;
+    const uint64_t full = 32ull * (kWbRows * kWbRows * u + kWbRows * (kWbRows - 1u) / 2u) * np;
+    const uint64_t J = 1024ull * bc + 32ull * (full - wnat) + (full - wrow);
+    cnt += C;
+    sum += (unsigned long long)C * a + 2ull * J;
+  } else {
+    uint32_t C = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) C += (uint32_t)__popc(pl[k]) << k;
+    cnt += C;
+  }
+#if SIEVE_WB_DIAG == 0
+  if (SIEVE_WB_WARP_COPY ? lane == 0 : threadIdx.x == 0) bulk_wait_read();
+#endif
+}
+
 constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;  // look-back flag states (A2 K1, A8 list)
 
 // A8 (list mode): the primes of one segment (natural layout, after
@@ -1626,16 +1901,22 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       }
       __syncthreads();
     } else if (MODE == kList) {
-      untranspose(seg, valid);
+      if (SIEVE_REG_TRANSPOSE) untranspose_reg(seg, valid);
+      else untranspose(seg, valid);
       __syncthreads();
       cnt += list_emit(seg, s, a, valid, P, s_wc, &s_off);
     } else {
-      if (MODE == kBitmap) {
-        if (SIEVE_WB_DIAG != 3) untranspose<true>(seg, valid);
-        if (SIEVE_TMA_STORE) fence_proxy_async_smem();
-        __syncthreads();
+      if (MODE == kBitmap && SIEVE_WB_FUSED) {
+        if (P.flags & kFlagNoSum) writeback_fused<false>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
+        else writeback_fused<true>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
+      } else {
+        if (MODE == kBitmap) {
+          if (SIEVE_WB_DIAG != 3) untranspose<true>(seg, valid);
+          if (SIEVE_TMA_STORE) fence_proxy_async_smem();
+          __syncthreads();
+        }
+        epilogue<MODE>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
       }
-      epilogue<MODE>(seg, a, bit0, valid, P.out, P.out_words, P.out_vec4, cnt, sum);
       __syncthreads();
     }
     if (P.prof && threadIdx.x == 0) {  // CTA-level phase cycles (diagnostics only)
@@ -1647,7 +1928,9 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
     }
   }
   if (MODE == kBatch) return;
-  if (MODE == kBitmap && SIEVE_TMA_STORE && threadIdx.x == 0) bulk_wait_all();
+  if (MODE == kBitmap && SIEVE_TMA_STORE &&
+      ((SIEVE_WB_FUSED && SIEVE_WB_WARP_COPY) ? (threadIdx.x & 31u) == 0 : threadIdx.x == 0))
+    bulk_wait_all();
 
   // per-CTA partial added into the launch's accumulator (u64 atomics: exact
   // mod 2^64, so the order does not matter); the last CTA to finish takes
@@ -1684,7 +1967,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
         sm = t.y;
       }
       P.result[0] = c;
-      P.result[1] = sm;
+      P.result[1] = (MODE == kBitmap && (P.flags & kFlagNoSum)) ? 0ull : sm;
       *P.done = 0u;  // ready for the next launch
       if (P.gbar) *P.gbar = 0u;  // every CTA is past both grid barriers
       if (P.prof) atomicMax(P.prof + 108, global_ns());

@@ -490,9 +490,10 @@ int stats_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, c
 }
 
 int bitmap_async(const Plan &P, const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase,
-                 uint32_t *out, uint64_t *result, const BaseReq *req) {
+                 uint32_t *out, uint64_t *result, const BaseReq *req, bool want_sum) {
   if (P.nbits == 0) return stats_async(P, primes, recips, nbase, result, req);
   sv::SieveParams sp = params_for(P, primes, recips, nbase, result);
+  if (!want_sum) sp.flags |= sv::kFlagNoSum;
   sp.out = out;
   sp.out_words = P.words;
   sp.out_vec4 = ((uintptr_t)out & 15u) == 0 ? 1u : 0u;
@@ -598,7 +599,7 @@ int64_t do_bitmap(uint64_t lo, uint64_t hi, uint32_t *out) {
     TRY(g.bitmap.ensure(P.words));
     dst = g.bitmap.p;
   }
-  TRY(bitmap_async(P, q.primes, q.recips, q.nbase, dst, g.result.p, &q));
+  TRY(bitmap_async(P, q.primes, q.recips, q.nbase, dst, g.result.p, &q, false));
   if (!dev)
     CUDA_TRY(cudaMemcpyAsync(out, dst, P.words * 4, cudaMemcpyDeviceToHost, g.stream()));
   uint64_t c = 0;
@@ -889,7 +890,7 @@ int sieve_bitmap_async(uint64_t lo, uint64_t hi, const uint32_t *primes, const u
   const Plan P = make_plan(lo, hi);
   if (P.words && !out) return fail(SIEVE_EINVAL, "NULL out");
   TRY(ensure_ready());
-  return bitmap_async(P, primes, recips, nbase, out, result, nullptr);
+  return bitmap_async(P, primes, recips, nbase, out, result, nullptr, !g.opt.bitmap_count_only);
 }
 
 int sieve_bitmap_base_async(uint64_t lo, uint64_t hi, uint32_t *primes, uint64_t *recips,
@@ -903,7 +904,7 @@ int sieve_bitmap_base_async(uint64_t lo, uint64_t hi, uint32_t *primes, uint64_t
                                             (unsigned long long)cap, (unsigned long long)P.r);
   TRY(ensure_ready());
   const BaseReq q{primes, recips, nbase, cap, P.r};
-  return bitmap_async(P, primes, recips, nbase, out, result, &q);
+  return bitmap_async(P, primes, recips, nbase, out, result, &q, !g.opt.bitmap_count_only);
 }
 
 int sieve_peer_slab_handle(void *handle_out) {
@@ -1043,8 +1044,11 @@ int sieve_set_options(const sieve_options *o) {
   sieve_options n;
   default_options(n);
   if (o) {
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 2; ++i)
       if (o->reserved[i]) return fail(SIEVE_EINVAL, "reserved option fields must be zero");
+    if (o->bitmap_count_only > 1)
+      return fail(SIEVE_EINVAL, "bitmap_count_only %u not in {0, 1}", o->bitmap_count_only);
+    n.bitmap_count_only = o->bitmap_count_only;
     if (o->buckets > 1) return fail(SIEVE_EINVAL, "buckets %u not in {0, 1}", o->buckets);
     n.buckets = o->buckets;
     if (o->segment_kb) {

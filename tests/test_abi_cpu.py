@@ -50,9 +50,13 @@ def test_validation_before_device():
     with pytest.raises(sv.SieveError):
         sv.set_options(segment_kb=208, wheel=47)  # 208 KiB + 25 KiB of tables > 226 KiB
     assert sv.get_options()["segment_kb"] == 64
+    with pytest.raises(sv.SieveError):
+        sv.set_options(bitmap_count_only=2)
+    sv.set_options(bitmap_count_only=1)
+    assert sv.get_options()["bitmap_count_only"] == 1
     sv.set_options()
     assert sv.get_options() == {"segment_kb": 208, "wheel": 31, "ctas_per_sm": 0, "threads": 1024,
-                                 "buckets": 0}
+                                 "buckets": 0, "bitmap_count_only": 0}
 
 
 def test_no_cpu_fallback_without_gpu():

@@ -610,3 +610,39 @@ def test_full_size_bitmaps_sampled_windows(cfg):
         assert np.array_equal(w[w0:w1], obm), (cfg, w0)
     del out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("count_only", [0, 1])
+@pytest.mark.parametrize("seg_kb,threads", [(208, 1024), (64, 256), (32, 512), (8, 1024)])
+def test_bitmap_async_sum_and_count_only(count_only, seg_kb, threads):
+    """The fused write-back (in-register half-block transpose, count and
+    prime sum from the rows and words it holds) against the oracle on ranges
+    that span several segments, ragged tails, outputs at 4-byte offsets (no
+    bulk copy) and every thread count: with the sum (result = (count, sum))
+    and with the option bitmap_count_only (carry-save count, result[1] = 0)."""
+    torch = pytest.importorskip("torch")
+    from paper_1205_4883_b200 import dist as D
+    sv.set_options(segment_kb=seg_kb, threads=threads, bitmap_count_only=count_only)
+    g = inputs.SplitMix64(77 + seg_kb)
+    ranges = [(0, 3 * 10**7 + 17), (10**12 + 3, 10**12 + 2 * 10**7 + 1), (2, 1025), (2, 64 * 1024 * 33 + 5)]
+    ranges += [(a, a + 1 + g.next() % (3 * 10**6)) for a in (10**9 + g.next() % 10**9 for _ in range(4))]
+    sv.set_stream(torch.cuda.current_stream())
+    try:
+        for lo, hi in ranges:
+            r = D.isqrt(hi - 1)
+            base = D.alloc_base(sv.base_capacity(r), torch.device("cuda"))
+            words = sv.bitmap_words(lo, hi)
+            obm, oc, os_ = oracle.bitmap(lo, hi)
+            for shift in (0, 1):  # 16-byte aligned output (bulk copies) and a 4-byte offset
+                buf = torch.zeros(words + 4, dtype=torch.int32, device="cuda")
+                out = buf[shift:shift + words]
+                res = torch.zeros(2, dtype=torch.int64, device="cuda")
+                sv.bitmap_base_async(lo, hi, base.primes, base.recips, base.nbase, out, res)
+                torch.cuda.synchronize()
+                c, s = (int(x) & MASK64 for x in res.cpu().tolist())
+                assert c == oc, (lo, hi, shift)
+                assert s == (0 if count_only else os_), (lo, hi, shift)
+                assert np.array_equal(out.cpu().numpy().view(np.uint32), obm), (lo, hi, shift)
+                assert int(buf[:shift].abs().sum()) == 0 and int(buf[shift + words:].abs().sum()) == 0
+    finally:
+        sv.set_stream(None)

@@ -131,6 +131,15 @@ def config2(opts, lohi=None, tag=2):
     sv.debug_set_flags(1)
     wmed, wmn = timed(lambda: sv.bitmap_base_async(lo, hi, b.primes, b.recips, b.nbase, out, res))
     sv.debug_set_flags(0)
+    # the same calls returning the count only (option bitmap_count_only: no prime sum, the
+    # configs' "bitmap + count"; sieve_bitmap's own path)
+    sv.set_options(**{**sv.get_options(), "bitmap_count_only": 1})
+    cmed, _ = timed(lambda: sv.bitmap_base_async(lo, hi, b.primes, b.recips, b.nbase, out, res))
+    ok = ok and res.cpu().tolist()[0] == want
+    sv.debug_set_flags(1)
+    cwmed, _ = timed(lambda: sv.bitmap_base_async(lo, hi, b.primes, b.recips, b.nbase, out, res))
+    sv.debug_set_flags(0)
+    sv.set_options(**{**sv.get_options(), "bitmap_count_only": 0})
     byts = words * 4
     emit({"config": tag, "mode": "bitmap", "segment_kb": seg_kb, "ok": ok, "kernel_ms": med,
           "integers_per_s": (hi - lo) / (med / 1e3), "bitmap_bytes": byts,
@@ -139,6 +148,9 @@ def config2(opts, lohi=None, tag=2):
           "hbm_frac_end_to_end": byts / (med / 1e3) / 1e9 / HBM_PEAK,
           "writeback_only_ms": wmed, "writeback_only_gbs": byts / (wmed / 1e3) / 1e9,
           "writeback_only_frac": byts / (wmed / 1e3) / 1e9 / HBM_PEAK,
+          "count_only_kernel_ms": cmed, "count_only_hbm_frac_end_to_end": byts / (cmed / 1e3) / 1e9 / HBM_PEAK,
+          "count_only_writeback_only_ms": cwmed,
+          "count_only_writeback_only_frac": byts / (cwmed / 1e3) / 1e9 / HBM_PEAK,
           "hbm_peak_gbs": HBM_PEAK, "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy)",
           "call": "sieve_bitmap_base_async (fused A2 + sieve + write-back, one launch)"})
     del out

@@ -21,6 +21,9 @@ __global__ void k(uint32_t *out, uint32_t iters, uint32_t m) {
       if (OP == 5) asm volatile("min.u32 %0, %0, %1;" : "+r"(x[i]) : "r"(m));
       if (OP == 6) asm volatile("{ .reg .pred q; setp.lt.u32 q, %0, %1; @q add.u32 %0, %0, 1; }" : "+r"(x[i]) : "r"(m));
       if (OP == 7) asm volatile("shr.b32 %0, %0, 5;" : "+r"(x[i]));
+      if (OP == 8) asm volatile("popc.b32 %0, %0;" : "+r"(x[i]));
+      if (OP == 9) asm volatile("shfl.sync.bfly.b32 %0, %0, 1, 31, -1;" : "+r"(x[i]));
+      if (OP == 10) asm volatile("{ .reg .u32 t; popc.b32 t, %0; add.u32 %0, %0, t; }" : "+r"(x[i]));
     }
   }
   uint32_t s = 0;
@@ -32,13 +35,13 @@ __global__ void k(uint32_t *out, uint32_t iters, uint32_t m) {
 int main() {
   uint32_t *out;
   cudaMalloc(&out, 4);
-  const char *names[] = {"lop3", "shf.l.wrap", "mad.lo", "mad.hi", "add", "min", "setp+@p add", "shr"};
+  const char *names[] = {"lop3", "shf.l.wrap", "mad.lo", "mad.hi", "add", "min", "setp+@p add", "shr", "popc", "shfl.bfly", "popc+add"};
   int nsm = 148, clk = 0;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const uint32_t iters = 1 << 14;
-  for (int op = 0; op < 8; ++op) {
+  for (int op = 0; op < 11; ++op) {
     void (*f)(uint32_t *, uint32_t, uint32_t) =
-        op == 0 ? k<0> : op == 1 ? k<1> : op == 2 ? k<2> : op == 3 ? k<3> : op == 4 ? k<4> : op == 5 ? k<5> : op == 6 ? k<6> : k<7>;
+        op == 0 ? k<0> : op == 1 ? k<1> : op == 2 ? k<2> : op == 3 ? k<3> : op == 4 ? k<4> : op == 5 ? k<5> : op == 6 ? k<6> : op == 7 ? k<7> : op == 8 ? k<8> : op == 9 ? k<9> : k<10>;
     f<<<nsm * 2, 512>>>(out, 16, 3u);
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);

@@ -10,7 +10,7 @@ from paper_1205_4883_b200 import dist as D
 dev = torch.device("cuda", 0)
 stream = torch.cuda.Stream(); sv.set_stream(stream); torch.cuda.set_stream(stream)
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-lo, hi = inputs.CONFIG2
+lo, hi = inputs.CONFIG3 if 'c3' in sys.argv[1:] else inputs.CONFIG2
 r = math.isqrt(hi - 1)
 b = D.alloc_base(sv.base_capacity(r), dev)
 sv.base_primes_async(r, b.primes, b.recips, b.nbase)
