@@ -268,7 +268,9 @@ int sieve_debug_set_profile(uint64_t *dev_counters);
  * launch path the library falls back to when a cooperative launch is
  * refused; results must not change); 64 = count mode through the F3
  * cluster-pair kernel (two CTAs per super-segment, the large primes over
- * distributed shared memory; an A/B variant, results must not change).
+ * distributed shared memory; an A/B variant, results must not change);
+ * 256 = skip the wheel init as well (with 1: the bitmap transpose, count and
+ * copy alone; results WRONG).
  * 0 restores. */
 int sieve_debug_set_flags(uint32_t flags);
 

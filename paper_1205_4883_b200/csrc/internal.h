@@ -270,6 +270,9 @@ constexpr uint32_t kFlagCluster = 64u;
 // the write-back counts from carry-save planes only; result[1] = 0.  A
 // product flag, set by the runtime -- not a diagnostic.
 constexpr uint32_t kFlagNoSum = 128u;
+// Diagnostic flag: skip the wheel init too (with kFlagSkipMarking: the
+// bitmap write-back -- transpose, count, copy -- alone).  Results are wrong.
+constexpr uint32_t kFlagSkipWheel = 256u;
 
 enum Mode { kCount = 0, kBitmap = 1, kBatch = 2, kList = 3 };
 

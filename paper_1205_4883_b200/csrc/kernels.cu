@@ -1880,7 +1880,8 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       a = o0 + 2ull * bit0;
     }
     const long long c0 = P.prof ? clock64() : 0;
-    if (!(pre_init && s_it == s_begin)) wheel_init<NG, kWheelUnrollOf>(seg, tab, o0, bit0, valid, a);
+    if (!(pre_init && s_it == s_begin) && !(MODE == kBitmap && (P.flags & kFlagSkipWheel)))
+      wheel_init<NG, kWheelUnrollOf>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
     if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch ? kPlainILP : kPlain ? kPlainILPCount : 0>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);

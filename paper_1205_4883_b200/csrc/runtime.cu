@@ -1151,7 +1151,7 @@ int sieve_is_prime(const uint64_t *nums, uint64_t n, uint8_t *out) {
 int sieve_debug_set_flags(uint32_t flags) {
   std::lock_guard<std::mutex> lk(g.mu);
   if (flags & ~(sv::kFlagSkipMarking | sv::kFlagSkipA | sv::kFlagSkipB | sv::kFlagSkipC |
-                sv::kFlagReverse | sv::kFlagNoCoop | sv::kFlagCluster))
+                sv::kFlagReverse | sv::kFlagNoCoop | sv::kFlagCluster | sv::kFlagSkipWheel))
     return fail(SIEVE_EINVAL, "unknown debug flags %u", flags);
   g.flags = flags;
   return 0;

@@ -138,7 +138,13 @@ def config2(opts, lohi=None, tag=2):
     ok = ok and res.cpu().tolist()[0] == want
     sv.debug_set_flags(1)
     cwmed, _ = timed(lambda: sv.bitmap_base_async(lo, hi, b.primes, b.recips, b.nbase, out, res))
+    sv.debug_set_flags(1 | 256)  # wheel init skipped too: transpose + count + bulk copy alone
+    ctmed, _ = timed(lambda: sv.bitmap_base_async(lo, hi, b.primes, b.recips, b.nbase, out, res))
     sv.debug_set_flags(0)
+    cmed_count = None
+    if tag == 3:  # the same range in count mode: the bitmap's marginal cost over count + sum
+        cres = torch.zeros(2, dtype=torch.int64, device=dev)
+        cmed_count, _ = timed(lambda: sv.stats_base_async(lo, hi, b.primes, b.recips, b.nbase, cres))
     sv.set_options(**{**sv.get_options(), "bitmap_count_only": 0})
     byts = words * 4
     emit({"config": tag, "mode": "bitmap", "segment_kb": seg_kb, "ok": ok, "kernel_ms": med,
@@ -151,6 +157,10 @@ def config2(opts, lohi=None, tag=2):
           "count_only_kernel_ms": cmed, "count_only_hbm_frac_end_to_end": byts / (cmed / 1e3) / 1e9 / HBM_PEAK,
           "count_only_writeback_only_ms": cwmed,
           "count_only_writeback_only_frac": byts / (cwmed / 1e3) / 1e9 / HBM_PEAK,
+          "transpose_copy_only_ms": ctmed, "transpose_copy_only_frac": byts / (ctmed / 1e3) / 1e9 / HBM_PEAK,
+          "count_mode_ms": cmed_count,
+          "marginal_vs_count_mode_frac": (byts / ((cmed - cmed_count) / 1e3) / 1e9 / HBM_PEAK)
+          if cmed_count and cmed > cmed_count else None,
           "hbm_peak_gbs": HBM_PEAK, "peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy)",
           "call": "sieve_bitmap_base_async (fused A2 + sieve + write-back, one launch)"})
     del out
