@@ -156,6 +156,9 @@ constexpr uint32_t kSmemAlign = 128;
 #ifndef SIEVE_WB_WARP_COPY  // fused write-back: one bulk copy per warp run (1) or per segment (0)
 #define SIEVE_WB_WARP_COPY 1
 #endif
+#ifndef SIEVE_PACK44  // batch plain pass: {p, floor(2^44/p)} in one load (1) or p + recip (0)
+#define SIEVE_PACK44 1
+#endif
 #ifndef SIEVE_WB_LANES  // lanes per 1024-slot block in the in-register transpose (2 or 4)
 #define SIEVE_WB_LANES 2
 #endif
@@ -246,6 +249,7 @@ struct SieveParams {
   uint32_t *bcounts;    // [gridDim.x] per-CTA prime counts, then [7] region boundaries
   unsigned int *gbar;   // grid barrier counter: 0 at launch, reset by the last CTA
   const uint32_t *nitems;  // batch mode, device-planned: the item count (overrides nseg)
+  const uint2 *pk44;       // batch mode: {p, floor(2^44/p)} per base prime (plain pass), or nullptr
 };
 
 // Diagnostic flag: skip step A4/A5 (wheel init + count/write-back only), to
@@ -289,6 +293,8 @@ cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64
                                uint32_t cap, uint32_t *nbase, uint64_t *flags, uint32_t epoch,
                                int nsm, unsigned long long *prof, cudaStream_t s);
 uint32_t base_slices(uint32_t r);  // look-back flags the base-prime kernel needs
+cudaError_t launch_pack44(const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase, uint2 *pk44,
+                          uint32_t cap, cudaStream_t s);
 cudaError_t launch_prepare(const uint32_t *primes, const uint32_t *nbase, uint64_t *recips,
                            uint32_t cap, cudaStream_t s);
 // A10 planning on the device (no host pass over the intervals): interval i

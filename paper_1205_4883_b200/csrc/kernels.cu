@@ -102,6 +102,17 @@ __device__ __forceinline__ uint32_t first_hit_scaled(uint32_t a_sh, uint32_t na_
   return min(j, j - p);
 }
 
+// first_hit_scaled with M = floor(2^(32+t)/p) given (the packed plain-pass
+// table holds floor(2^44/p); M = that >> (12 - t) for t <= 12).
+__device__ __forceinline__ uint32_t first_hit_m(uint32_t a_sh, uint32_t na_lo, uint32_t p, uint32_t M) {
+  const uint32_t d = (__umulhi(a_sh, M) + 3u) * p + na_lo;
+  uint32_t j2;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(j2) : "r"(d & 1u), "r"(p), "r"(d));
+  uint32_t j = j2 >> 1;
+  j = min(j, j - p);
+  return min(j, j - p);
+}
+
 // floor((2^64-1)/p) for an odd p >= 3, without a 64-bit integer division:
 // a double quotient (within 2^12 of the result), then the exact remainder
 // T = (2^64-1) - q p (|T| < 2^40, so mod-2^64 arithmetic gives it as a signed
@@ -364,7 +375,7 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
                                              const uint64_t *__restrict__ recips,
                                              const PrimeRegions R, uint32_t flags,
                                              uint64_t a, uint32_t valid, unsigned long long *prof,
-                                             const uint32_t *k15) {
+                                             const uint32_t *k15, const uint2 *__restrict__ pk44 = nullptr) {
   constexpr bool kPlainTwo = kPlainU > 0;
   // diagnostics (sieve_debug_set_flags): drop whole regions (wrong results)
   const uint32_t a1_end = flags & kFlagSkipA ? R.start : R.unit;
@@ -658,11 +669,55 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
       }
       return true;
     };
+    // batch kernel (pk44 != nullptr): {p, floor(2^44 / p)} in one 8-byte load
+    // per prime instead of 4 + 8 bytes in two loads, M = floor(2^44/p) >> (12 - t)
+    // (floors nest; needs a < 2^44 and every plain prime > 2^12, so that the
+    // quotient fits 32 bits)
+    const bool packed = pk44 != nullptr && scaled && t <= 12u && 4096u < __ldg(primes + two);
+    const uint32_t sh44 = 12u - t;
+    auto plain_pass_packed = [&](uint32_t k0, auto full) -> bool {
+      constexpr bool kFull = decltype(full)::value;
+      uint32_t pk[U], jk[U], kk[U], mk[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        kk[u] = k0 + u * blockDim.x + ((u & 1) ? blockDim.x - 1u - threadIdx.x : threadIdx.x);
+        const uint32_t k = kFull ? kk[u] : min(kk[u], c_end - 1u);
+        const uint2 v = __ldg(pk44 + k);
+        pk[u] = v.x;
+        mk[u] = v.y >> sh44;
+      }
+      if ((uint64_t)pk[U - 1] * pk[U - 1] <= a) {  // the largest of the pass: so for all
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t j = first_hit_m(a_sh, na_lo, pk[u], mk[u]);
+          jk[u] = (kFull || kk[u] < c_end) ? j : kFar;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t k = kFull ? kk[u] : min(kk[u], c_end - 1u);
+          const uint32_t j = first_hit(a, seg_end, pk[u], __ldg(recips + k));
+          jk[u] = ((!kFull && kk[u] >= c_end) || j == kNone) ? kFar : j;
+        }
+        if (jk[0] == kFar) return false;  // p^2 past the segment: so for every later prime
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t P4 = 4u * pk[u];
+        for (uint32_t J = 4u * jk[u] + 32u * sb; J < Jlim; J += P4) red_or(j_addr(J), j_mask(J));
+      }
+      return true;
+    };
     const uint32_t step = U * blockDim.x;
     uint32_t k0 = two;
     bool more = true;
-    for (; more && c_end - k0 >= step && k0 < c_end; k0 += step) more = plain_pass(k0, std::true_type{});
-    if (more && k0 < c_end) plain_pass(k0, std::false_type{});
+    if (packed) {
+      for (; more && c_end - k0 >= step && k0 < c_end; k0 += step) more = plain_pass_packed(k0, std::true_type{});
+      if (more && k0 < c_end) plain_pass_packed(k0, std::false_type{});
+    } else {
+      for (; more && c_end - k0 >= step && k0 < c_end; k0 += step) more = plain_pass(k0, std::true_type{});
+      if (more && k0 < c_end) plain_pass(k0, std::false_type{});
+    }
   }
   if (prof) {  // per-warp busy cycles of the regions (diagnostics only)
     const long long t4 = clock64();
@@ -1884,7 +1939,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       wheel_init<NG, kWheelUnrollOf>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
-    if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch ? kPlainILP : kPlain ? kPlainILPCount : 0>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15);
+    if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch ? kPlainILP : kPlain ? kPlainILPCount : 0>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15, MODE == kBatch ? P.pk44 : nullptr);
     if (buckets) {
       bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s_it), valid);
       bq = bq + 1u == P.ring ? 0u : bq + 1u;
@@ -2486,6 +2541,25 @@ cudaError_t launch_base_primes(uint32_t r, uint32_t rs, uint32_t *primes, uint64
   // all CTAs resident (the look-back waits on earlier slices): <= 4 per SM
   const uint32_t grid = ns < 4u * (uint32_t)nsm ? (ns ? ns : 1u) : 4u * (uint32_t)nsm;
   k_base_primes<<<grid, kBaseThreads, 0, s>>>(r, rs, primes, recips, cap, nbase, flags, epoch, prof);
+  return cudaGetLastError();
+}
+
+// batch plain pass: pk44[i] = {p_i, floor(2^44 / p_i)} (0 for p_i < 2^12,
+// where the quotient does not fit 32 bits and the packed pass is not used):
+// recip = floor((2^64 - 1) / p) = floor(2^64 / p) for odd p, and floors nest
+__global__ void k_pack44(const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase, uint2 *pk44,
+                         uint32_t cap) {
+  const uint32_t n = min(*nbase, cap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t p = primes[i];
+    pk44[i] = make_uint2(p, p > 4096u ? (uint32_t)(recips[i] >> 20) : 0u);
+  }
+}
+
+cudaError_t launch_pack44(const uint32_t *primes, const uint64_t *recips, const uint32_t *nbase, uint2 *pk44,
+                          uint32_t cap, cudaStream_t s) {
+  const int grid = (int)((cap + 255) / 256 < 1184 ? (cap + 255) / 256 : 1184);
+  k_pack44<<<grid > 0 ? grid : 1, 256, 0, s>>>(primes, recips, nbase, pk44, cap);
   return cudaGetLastError();
 }
 

@@ -124,6 +124,7 @@ struct Ctx {
   DevBuf<uint32_t> tables;
   DevBuf<uint32_t> primes;
   DevBuf<uint64_t> recips;
+  DevBuf<uint2> pk44;  // batch: {p, floor(2^44/p)} of the library-owned base primes
   DevBuf<uint32_t> nbase;
   DevBuf<uint64_t> partials;
   DevBuf<unsigned int> done;
@@ -680,6 +681,10 @@ int batch_async(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t hi_
   if (n * kcap > 0xFFFFFFFFull) return fail(SIEVE_EINVAL, "too many batch items");
   const uint64_t rmax = hi_max >= 2 ? isqrt_u64(hi_max - 1) : 0;
   TRY(own_base(rmax));
+  const uint64_t bcap = base_capacity(rmax);
+  TRY(g.pk44.ensure(bcap));
+  CUDA_TRY(sv::launch_pack44(g.primes.p, g.recips.p, g.nbase.p, g.pk44.p, (uint32_t)bcap, g.stream()));
+  g_launches += 1;
   if (!g.plan.p) {
     TRY(g.plan.ensure(2 * sv::kPlanBuckets));
     CUDA_TRY(cudaMemsetAsync(g.plan.p, 0, 2 * sv::kPlanBuckets * sizeof(uint32_t), g.stream()));
@@ -693,6 +698,7 @@ int batch_async(const uint64_t *lo, const uint64_t *hi, uint64_t n, uint64_t hi_
   sv::SieveParams sp = params_for(dummy, g.primes.p, g.recips.p, g.nbase.p, result);
   sp.items = g.items.p;
   sp.nitems = g.nitems.p;
+  sp.pk44 = SIEVE_PACK44 ? g.pk44.p : nullptr;
   sp.nseg = n * kcap;  // bound for the grid size; the kernel reads *nitems
   sp.r = (uint32_t)rmax;
   return run_sieve(sv::kBatch, sp, n * kcap);
@@ -1091,7 +1097,7 @@ void sieve_shutdown(void) {
   std::lock_guard<std::mutex> lk(g.mu);
   if (!g.ready) return;
   cudaStreamSynchronize(g.stream());
-  g.tables.release(); g.primes.release(); g.recips.release(); g.nbase.release();
+  g.tables.release(); g.primes.release(); g.recips.release(); g.pk44.release(); g.nbase.release();
   g.partials.release(); g.done.release(); g.result.release(); g.bitmap.release();
   g.list.release(); g.items.release(); g.bres.release();
   g.blo.release(); g.bhi.release(); g.plan.release(); g.nitems.release();
