@@ -249,7 +249,8 @@ struct SieveParams {
   uint32_t *bcounts;    // [gridDim.x] per-CTA prime counts, then [7] region boundaries
   unsigned int *gbar;   // grid barrier counter: 0 at launch, reset by the last CTA
   const uint32_t *nitems;  // batch mode, device-planned: the item count (overrides nseg)
-  const uint2 *pk44;       // batch mode: {p, floor(2^44/p)} per base prime (plain pass), or nullptr
+  uint2 *pk44;             // plain pass (batch and kPlain kernels): {p, floor(2^44/p)} per base
+                           // prime, or nullptr; written by the fused A2 when bprimes is set
 };
 
 // Diagnostic flag: skip step A4/A5 (wheel init + count/write-back only), to

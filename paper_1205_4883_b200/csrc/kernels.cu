@@ -1785,19 +1785,25 @@ __device__ __forceinline__ void base_phase(const SieveParams &P, uint32_t *seg) 
   }
   __syncthreads();
   const unsigned long long base = s_base;
+  // the plain pass's packed table (kPlain kernels): {p, floor(2^44 / p)}, k_pack44's rule
+  auto pack44 = [](uint32_t p, uint64_t q) { return make_uint2(p, p > 4096u ? (uint32_t)(q >> 20) : 0u); };
   if (tid < o && base + tid < P.bcap) {
     P.bprimes[base + tid] = p0;
     P.brecips[base + tid] = q0;
+    if (P.pk44) P.pk44[base + tid] = pack44(p0, q0);
   }
   if (t1 < o && base + t1 < P.bcap) {
     P.bprimes[base + t1] = p1;
     P.brecips[base + t1] = q1;
+    if (P.pk44) P.pk44[base + t1] = pack44(p1, q1);
   }
   for (uint32_t t = t1 + blockDim.x; t < o; t += blockDim.x) {  // large r only
     if (base + t < P.bcap) {
       const uint32_t p = stage[t];
+      const uint64_t q = recip_of(p);
       P.bprimes[base + t] = p;
-      P.brecips[base + t] = recip_of(p);
+      P.brecips[base + t] = q;
+      if (P.pk44) P.pk44[base + t] = pack44(p, q);
     }
   }
   if (P.prof && tid == 0) atomicMax(P.prof + 117, global_ns());
@@ -1939,7 +1945,7 @@ __global__ void __launch_bounds__(SIEVE_MAX_THREADS, 1) k_sieve(const SieveParam
       wheel_init<NG, kWheelUnrollOf>(seg, tab, o0, bit0, valid, a);
     __syncthreads();
     const long long c1 = P.prof ? clock64() : 0;
-    if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch ? kPlainILP : kPlain ? kPlainILPCount : 0>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15, MODE == kBatch ? P.pk44 : nullptr);
+    if (!(P.flags & kFlagSkipMarking)) mark_segment<MODE == kBatch ? kPlainILP : kPlain ? kPlainILPCount : 0>(sb, P.primes, P.recips, Ri, P.flags, a, valid, P.prof, s_k15, (MODE == kBatch || kPlain) ? P.pk44 : nullptr);
     if (buckets) {
       bucket_drain(P, bcnt, sb, bq, (uint32_t)(s_end - s_it), valid);
       bq = bq + 1u == P.ring ? 0u : bq + 1u;

@@ -434,6 +434,15 @@ int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork, const BaseReq *req =
   // together (round robin), a CTA's contiguous run would serialise it
   if (mode == sv::kCount || mode == sv::kBitmap) TRY(setup_buckets(sp, grid));
   const int ng = ng_for_wheel(g.opt.wheel);
+  // the kPlain kernels (launch_t: default wheel, r > S / kPlainHits) read the
+  // plain primes as {p, floor(2^44/p)} (written by the fused A2, else by k_pack44)
+  bool pack = false;
+  if (SIEVE_PACK44 && SIEVE_COUNT_PLAIN && mode != sv::kBatch && ng == SIEVE_PLAIN_NG &&
+      (uint64_t)sp.r > sp.seg_bits / SIEVE_PLAIN_HITS) {
+    TRY(g.pk44.ensure(base_capacity(sp.r)));
+    sp.pk44 = g.pk44.p;
+    pack = true;
+  }
   if (req) {
     sp.primes = req->primes;
     sp.recips = req->recips;
@@ -470,6 +479,11 @@ int run_sieve(int mode, sv::SieveParams sp, uint64_t nwork, const BaseReq *req =
     CUDA_TRY(sv::launch_sieve_cluster(ng, sp, grid, (int)g.opt.threads, sieve_smem(), g.stream()));
     g_launches += 1;
     return 0;
+  }
+  if (pack) {
+    CUDA_TRY(sv::launch_pack44(sp.primes, sp.recips, sp.nbase, sp.pk44, (uint32_t)base_capacity(sp.r),
+                               g.stream()));
+    g_launches += 1;
   }
   CUDA_TRY(sv::launch_sieve(ng, mode, sp, grid, (int)g.opt.threads, sieve_smem(), g.stream()));
   g_launches += 1;
