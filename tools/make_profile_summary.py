@@ -19,7 +19,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "gpurun_out")
-DST = os.path.join(ROOT, "profiles")
+DST = os.environ.get("PROFILE_DST", os.path.join(ROOT, "profiles"))
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 rep = os.path.join(SRC, sys.argv[2] if len(sys.argv) > 2 else "prof_sieve.ncu-rep")
 os.makedirs(DST, exist_ok=True)
