@@ -1,7 +1,8 @@
 // kernels.cu -- the sm_100a kernels of the segmented sieve of Eratosthenes.
 //
 // Steps:
-//   A2  k_base_primes : odd primes <= r (one CTA, chunked shared-memory sieve)
+//   A2  k_base_primes : odd primes <= r (sliced over CTAs, decoupled look-back),
+//                       or base_phase inside the sieve launch (fused A2)
 //   A3  wheel init    : segment <- OR of periodic composite patterns of 3..w
 //   A4  marking       : shared-memory atomicOr of the odd multiples of each
 //                       base prime w < p <= r, starting at max(p^2, first
@@ -13,7 +14,9 @@
 //                       lane-per-prime straight from their first hit, so a
 //                       segment a prime skips costs one Barrett reduction
 //   A6  count + sum   : popc of the inverted words, weighted popcs for the sum
-//   A7  bitmap        : 128-bit coalesced write-back of the inverted segment
+//   A7  bitmap        : writeback_fused: in-register transpose of each block,
+//                       count/sum from registers, prime words back to shared
+//                       memory, one TMA bulk copy per warp to HBM
 //   A8  list          : per-segment counts -> scan -> ballot/scan compaction
 //   A10 batch         : the same segment kernel over (interval, segment) items
 //

@@ -7,7 +7,8 @@
 // launch: the base primes (A2) are computed inside it (fused A2, a
 // cooperative launch with two grid barriers), then
 //   count  : A3-A6, the last CTA reduces the per-CTA (count, sum)
-//   bitmap : A3-A7, one TMA bulk copy of each segment's words to HBM
+//   bitmap : A3-A7, the fused write-back: in-register transpose, count,
+//            one TMA bulk copy per warp's 16 blocks to HBM
 //   primes : A3, A4/A5, A8 per-segment decoupled look-back + compaction
 // When the cooperative launch is not possible (a slice of the odd numbers
 // <= r does not fit a segment, or the launch is refused) the base-prime
