@@ -156,6 +156,9 @@ constexpr uint32_t kSmemAlign = 128;
 #ifndef SIEVE_WB_WARP_COPY  // fused write-back: one bulk copy per warp run (1) or per segment (0)
 #define SIEVE_WB_WARP_COPY 1
 #endif
+#ifndef SIEVE_B_PAIR  // region (B): pair hits 96 steps apart (one mask and one LOP3 per two atomics)
+#define SIEVE_B_PAIR 1
+#endif
 #ifndef SIEVE_PACK44  // batch plain pass: {p, floor(2^44/p)} in one load (1) or p + recip (0)
 #define SIEVE_PACK44 1
 #endif

@@ -496,6 +496,36 @@ __device__ __forceinline__ void mark_segment(uint32_t sb, const uint32_t *__rest
       uint32_t Q2 = Q1 + d * s4;
       uint32_t m2 = rotl(m1, d * p);
       const uint32_t s3 = 3u * s4, p3 = 3u * p;
+#if SIEVE_B_PAIR
+      // Paired blocks: hits 96 steps apart (96 = 0 mod 32 and mod 3) have the
+      // same bit (row + 96 p = row mod 32) and the same skip residue, and their
+      // byte offsets differ by D = 384 p, a multiple of 128: one mask rotation
+      // and one LOP3 serve two atomics, the second address is one add.  Each
+      // block marks steps [0, 96) and [96, 192) of the lane's walk in 16
+      // iterations, then skips the 96 steps its second stream covered (the
+      // masks rotate by 32 x 3p = 0 mod 32 per block: unchanged).  Only whole
+      // blocks inside the segment; the loop below takes the rest.
+      const uint32_t D = 32u * s3;
+      for (; Q2 + 31u * s3 + D < Qlim; Q1 += D, Q2 += D) {
+#pragma unroll 2
+        for (int c = 0; c < 16; ++c, Q1 += 2u * s3, Q2 += 2u * s3) {
+          const uint32_t a1 = (Q1 & ~127u) | b4, a2 = (Q2 & ~127u) | b4;
+          red_or(a1, m1);
+          red_or(a1 + D, m1);
+          red_or(a2, m2);
+          red_or(a2 + D, m2);
+          m1 = rotl(m1, p3);
+          m2 = rotl(m2, p3);
+          const uint32_t a3 = ((Q1 + s3) & ~127u) | b4, a4 = ((Q2 + s3) & ~127u) | b4;
+          red_or(a3, m1);
+          red_or(a3 + D, m1);
+          red_or(a4, m2);
+          red_or(a4 + D, m2);
+          m1 = rotl(m1, p3);
+          m2 = rotl(m2, p3);
+        }
+      }
+#endif
       for (; Q2 + s3 < Qlim; Q1 += 2u * s3, Q2 += 2u * s3) {
         red_or((Q1 & ~127u) | b4, m1);
         red_or((Q2 & ~127u) | b4, m2);
