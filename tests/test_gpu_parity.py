@@ -142,6 +142,14 @@ def test_thread_and_occupancy_invariance(threads):
     sv.set_options(threads=threads, segment_kb=64, ctas_per_sm=2)
     lo, hi = 10**11, 10**11 + 5 * 10**7 + 3
     assert sv.stats(lo, hi) == oracle.stats(lo, hi)
+    # the write-back and list paths at every thread count (in-register
+    # transpose: 2 lanes per block, tail lanes duplicating the last block)
+    lo, hi = 10**11 + 7, 10**11 + 2 * 10**7 + 5
+    obm, oc, _ = oracle.bitmap(lo, hi)
+    bm, c = sv.bitmap(lo, hi)
+    assert c == oc and np.array_equal(bm, obm)
+    lst, c = sv.primes(lo, hi)
+    assert c == oc and np.array_equal(lst, oracle.primes(lo, hi))
 
 
 def test_primes_list_truncation_and_device_out():
