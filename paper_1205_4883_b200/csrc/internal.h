@@ -63,7 +63,7 @@ constexpr uint64_t kOddPrimesBelow64 =
 #endif
 constexpr uint32_t kUnitHits = SIEVE_UNIT_HITS;
 #ifndef SIEVE_CLASS_HITS
-#define SIEVE_CLASS_HITS 24576  // A/B-tuned with the 3-skip (16384 -> 24576)
+#define SIEVE_CLASS_HITS 28672  // A/B-tuned: 16384 -> 24576 with the 3-skip, -> 28672 with the paired (B) blocks
 #endif
 constexpr uint32_t kClassHits = SIEVE_CLASS_HITS;
 #ifndef SIEVE_A2_PARTS
