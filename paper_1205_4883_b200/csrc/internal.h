@@ -98,7 +98,7 @@ constexpr uint32_t kPlainHits = SIEVE_PLAIN_HITS;
 #endif
 constexpr int kPlainILP = SIEVE_PLAIN_ILP;
 #ifndef SIEVE_PLAIN_ILP_COUNT  // the same pass in the count/bitmap/list kernels of large r
-#define SIEVE_PLAIN_ILP_COUNT 8  // config 4: 2 -> 1.782, 4 -> 1.761, 8 -> 1.751 ms
+#define SIEVE_PLAIN_ILP_COUNT 4  // config 4: 2 -> 1.782, 4 -> 1.761, 8 -> 1.751 ms; with the packed table 2 / 4 / 6 / 8 -> 1.666 / 1.625 / 1.635 / 1.644 ms
 #endif
 #ifndef SIEVE_PLAIN_NG  // the wheel (groups) for which the plain-pass kernels are instantiated
 #define SIEVE_PLAIN_NG 4
