@@ -395,6 +395,12 @@ def main():
     if world > 1:
         tdist.all_reduce(tot, op=tdist.ReduceOp.MAX)
     ms_per_step = tot[0].item() / args.steps
+    # the per-step distribution (each step's time the max
+    # over ranks), median / min / max next to the mean
+    per = torch.tensor(step_ms, dtype=torch.float64, device=dev)
+    if world > 1:
+        tdist.all_reduce(per, op=tdist.ReduceOp.MAX)
+    per = per.tolist()
     sieve_ms_mean = tot[1].item() / args.steps
     value = (hi - lo) / (ms_per_step / 1e3)
 
@@ -461,6 +467,8 @@ def main():
                                      "fused in the sieve kernel (NVLink peer memory)" if fused
                                      else "NCCL all_reduce")},
             "verified": verified,
+            "step_ms": {"median": statistics.median(per), "min": min(per), "max": max(per),
+                        "n": len(per), "note": "per timed step, max over ranks (CUDA events)"},
             "base_ms": statistics.mean(base_ms),
             "wall_ms_per_step_incl_flush": t_wall * 1e3 / args.steps,
             "roofline": roof,

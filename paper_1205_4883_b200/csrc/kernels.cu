@@ -1375,7 +1375,7 @@ constexpr uint64_t kFlagAgg = 1, kFlagIncl = 2;  // look-back flag states (A2 K1
 // of the segment's words; pass 1 counts its primes; thread 0 publishes the
 // segment's count, finds the segment's place in the list by a decoupled
 // look-back over the earlier segments, and publishes its inclusive prefix;
-// pass 2 has the lanes of a warp take 32 consecutive words at a time, place
+// pass 2 has the lanes of a warp take 32 x SIEVE_LIST_WORDS consecutive words at a time, place
 // them by a warp scan of their popcounts, and write their primes.  Returns
 // the segment's count in thread 0 (0 elsewhere).
 __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, uint64_t a,
@@ -1438,10 +1438,19 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
   }
   __syncthreads();
   unsigned long long base = *s_off + s_wc[warp];
-  for (uint32_t w0 = wb; w0 < we; w0 += 32u) {
-    const uint32_t w = w0 + lane;
-    uint32_t x = w < we ? ~seg[w] : 0u;
-    const uint32_t cx = __popc(x);
+  // lane l takes kLW consecutive words per pass (one scan and one set of
+  // 64-bit offsets per kLW words); their primes go out word by word
+  constexpr uint32_t kLW = SIEVE_LIST_WORDS;
+  static_assert(kLW >= 1 && kLW <= 4, "SIEVE_LIST_WORDS: 1 to 4");
+  for (uint32_t w0 = wb; w0 < we; w0 += 32u * kLW) {
+    const uint32_t w = w0 + kLW * lane;
+    uint32_t xs[kLW];
+    uint32_t cx = 0;
+#pragma unroll
+    for (uint32_t e = 0; e < kLW; ++e) {
+      xs[e] = w + e < we ? ~seg[w + e] : 0u;
+      cx += __popc(xs[e]);
+    }
     uint32_t incl = cx;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1450,34 +1459,43 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
     }
     unsigned long long k = base + incl - cx;
     const uint64_t v0 = a + 64ull * w;
-    if (k + cx <= P.list_cap) {  // the whole word fits: no per-prime check
+    if (k + cx <= P.list_cap) {  // the lane's words fit: no per-prime check
       // two primes per 16-byte store once the address is 16-byte aligned:
       // the emission is bound by the number of store instructions
       uint64_t *dst = P.list + k;
       SV_CHECK(k + cx <= P.list_cap, kVioListStore);
-      if ((reinterpret_cast<uintptr_t>(dst) & 8u) && x) {
-        *dst++ = v0 + 2ull * (uint32_t)(__ffs(x) - 1);
-        x &= x - 1;
-      }
-      while (x) {
-        const uint32_t b1 = __ffs(x) - 1;
-        x &= x - 1;
-        if (x) {
-          const uint32_t b2 = __ffs(x) - 1;
+#pragma unroll
+      for (uint32_t e = 0; e < kLW; ++e) {
+        uint32_t x = xs[e];
+        const uint64_t ve = v0 + 64ull * e;
+        if ((reinterpret_cast<uintptr_t>(dst) & 8u) && x) {
+          *dst++ = ve + 2ull * (uint32_t)(__ffs(x) - 1);
           x &= x - 1;
-          SV_CHECK(dst + 2 <= P.list + P.list_cap && ((uintptr_t)dst & 15u) == 0, kVioListStore);
-          *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(v0 + 2ull * b1, v0 + 2ull * b2);
-          dst += 2;
-        } else {
-          *dst++ = v0 + 2ull * b1;
+        }
+        while (x) {
+          const uint32_t b1 = __ffs(x) - 1;
+          x &= x - 1;
+          if (x) {
+            const uint32_t b2 = __ffs(x) - 1;
+            x &= x - 1;
+            SV_CHECK(dst + 2 <= P.list + P.list_cap && ((uintptr_t)dst & 15u) == 0, kVioListStore);
+            *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(ve + 2ull * b1, ve + 2ull * b2);
+            dst += 2;
+          } else {
+            *dst++ = ve + 2ull * b1;
+          }
         }
       }
     } else {
-      while (x) {
-        const uint32_t b = __ffs(x) - 1;
-        x &= x - 1;
-        if (k < P.list_cap) P.list[k] = v0 + 2ull * b;
-        ++k;
+#pragma unroll
+      for (uint32_t e = 0; e < kLW; ++e) {
+        uint32_t x = xs[e];
+        while (x) {
+          const uint32_t b = __ffs(x) - 1;
+          x &= x - 1;
+          if (k < P.list_cap) P.list[k] = v0 + 64ull * e + 2ull * b;
+          ++k;
+        }
       }
     }
     base += __shfl_sync(0xffffffffu, incl, 31);
