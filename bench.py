@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--broadcast", action="store_true",
                     help="rank 0 computes the base primes and NCCL-broadcasts them (default: every "
                          "rank recomputes them, 18 us for config 3 -- no collective on the path)")
+    ap.add_argument("--split", choices=["equal", "cost"], default="equal",
+                    help="N>1 block split: equal contiguous blocks (config 3, default) or "
+                         "cost-weighted blocks (dist.block_of split='cost')")
     ap.add_argument("--allreduce", choices=["fused", "nccl"], default="fused",
                     help="N>1: the (count, sum) all-reduce inside the sieve kernel over NVLink peer "
                          "memory (F4, csrc/peer.cuh; falls back to nccl on every rank if any rank "
@@ -303,7 +306,7 @@ def main():
     r = math.isqrt(hi - 1)
     base = D.alloc_base(sv.base_capacity(r), dev)
     result = torch.zeros(2, dtype=torch.int64, device=dev)
-    a, b = D.block_of(lo, hi, rank, world)
+    a, b = D.block_of(lo, hi, rank, world, args.split)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
     bcast = world > 1 and args.broadcast
     fused = world > 1 and args.allreduce == "fused"
@@ -462,7 +465,7 @@ def main():
                        "lo": lo, "hi": hi, "segment_kb": opts["segment_kb"], "wheel": opts["wheel"],
                        "threads": opts["threads"], "base_primes": "rank 0 + NCCL broadcast" if bcast else "per rank, fused into the sieve launch",
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
-                       "parallelism": f"range split over {world} GPU(s)",
+                       "parallelism": f"range split over {world} GPU(s)" + (f", {args.split} blocks" if world > 1 else ""),
                        "allreduce": ("none" if world == 1 else
                                      "fused in the sieve kernel (NVLink peer memory)" if fused
                                      else "NCCL all_reduce")},

@@ -37,23 +37,57 @@ def isqrt(x: int) -> int:
     return math.isqrt(x) if x > 0 else 0
 
 
-def block_of(lo: int, hi: int, rank: int, world: int) -> tuple[int, int]:
-    """Step A1 across GPUs (reading R10): block `rank` of `world` equal
-    contiguous blocks of [lo, hi) on the odd-only word grid.  Boundaries sit
-    at o0 + 64*floor(k*words/world) (o0 = lo|1), clipped to [lo, hi], so
-    every block's bitmap starts on a 32-bit word of the whole range's bitmap
-    and the blocks tile [lo, hi) exactly."""
+# Cost-weighted split (split="cost"): marking work per integer near x grows
+# like sum_{w < p <= sqrt(x)} 1/p ~ ln ln x + const (Mertens), so equal blocks
+# of [2, 10^10] leave the top rank ~19 % more kernel time than rank 0 at G = 8
+# (profiles/r02_rank_blocks.txt).  COST_KAPPA is the constant of the density
+# ln ln x - kappa fitted to those block times on B200 (default segment size,
+# wheel 31); only the ratio of the densities at the two ends matters.
+COST_KAPPA = 2.35
+_COST_FLOOR = 0.05
+_COST_PANELS = 4096
+
+
+def _cost_edges(lo: int, hi: int, world: int, words: int) -> list[int]:
+    """Word indices k_1 <= ... <= k_{world-1} cutting [lo, hi) into `world`
+    pieces of equal modelled cost (midpoint rule on _COST_PANELS panels,
+    inverted by linear interpolation; the same on every rank)."""
+    n = _COST_PANELS
+    x = lo + (np.arange(n, dtype=np.float64) + 0.5) * ((hi - lo) / n)
+    dens = np.maximum(np.log(np.log(np.maximum(x, 16.0))) - COST_KAPPA, _COST_FLOOR)
+    cum = np.concatenate([[0.0], np.cumsum(dens)])
+    cum /= cum[-1]
+    pos = np.interp(np.arange(1, world) / world, cum, np.arange(n + 1) / n)
+    ks = [min(words, max(0, int(round(float(f) * words)))) for f in pos]
+    for i in range(1, len(ks)):
+        ks[i] = max(ks[i], ks[i - 1])
+    return ks
+
+
+def block_of(lo: int, hi: int, rank: int, world: int, split: str = "equal") -> tuple[int, int]:
+    """Step A1 across GPUs (reading R10): block `rank` of `world` contiguous
+    blocks of [lo, hi) on the odd-only word grid.  split="equal" (default,
+    PAPER.md:19 "average divide data into nodes", config 3): boundaries at
+    o0 + 64*floor(k*words/world) (o0 = lo|1), clipped to [lo, hi].
+    split="cost": boundaries at words of equal modelled marking cost
+    (_cost_edges; the load balance PAPER.md:105-110 asks for, applied across
+    GPUs).  Either way every block's bitmap starts on a 32-bit word of the
+    whole range's bitmap and the blocks tile [lo, hi) exactly."""
+    if split not in ("equal", "cost"):
+        raise ValueError(f"split must be 'equal' or 'cost', not {split!r}")
     if hi <= lo:
         return lo, hi
     o0 = lo | 1
     words = (hi // 2 - lo // 2 + 31) // 32
+    cost = _cost_edges(lo, hi, world, words) if split == "cost" and world > 1 else None
 
     def edge(k: int) -> int:
         if k <= 0:
             return lo
         if k >= world:
             return hi
-        return min(hi, o0 + 64 * ((k * words) // world))
+        kw = cost[k - 1] if cost is not None else (k * words) // world
+        return min(hi, o0 + 64 * kw) if kw > 0 else lo
 
     return edge(rank), edge(rank + 1)
 
@@ -222,12 +256,14 @@ def detach_peers(group=None, backend=None) -> None:
 
 
 def stats(lo: int, hi: int, group=None, broadcast: bool = True, base: BaseBuffers | None = None,
-          result=None, sync: bool = True, backend=None, device=None, fused: bool | None = None):
+          result=None, sync: bool = True, backend=None, device=None, fused: bool | None = None,
+          split: str = "equal"):
     """pi-count and prime sum of [lo, hi) over all ranks of `group` (public
     multi-GPU API).  Returns (count, sum mod 2^64) on every rank when sync,
     else the device result tensor (int64[2], already all-reduced).
     fused (default: whether attach_peers(group) was done): the all-reduce
-    runs inside the sieve kernel over peer memory (F4) instead of NCCL."""
+    runs inside the sieve kernel over peer memory (F4) instead of NCCL.
+    split: "equal" blocks (config 3) or "cost"-weighted blocks (block_of)."""
     import torch
     import torch.distributed as dist
 
@@ -240,7 +276,7 @@ def stats(lo: int, hi: int, group=None, broadcast: bool = True, base: BaseBuffer
         base = alloc_base(be.base_capacity(r), dev)
     if result is None:
         result = torch.zeros(2, dtype=torch.int64, device=dev)
-    a, b = block_of(lo, hi, rank, world)
+    a, b = block_of(lo, hi, rank, world, split)
     if fused is None:
         fused = _ATTACHED.get(id(group)) == world
     if world > 1 and broadcast:

@@ -136,6 +136,7 @@ def _worker(rank, world, port, q, tmpdir=None):
                        (2**63 // 2**16, 2**63 // 2**16 + 10**5)]:
             out[(lo, hi)] = D.stats(lo, hi, backend=be, device=cpu)
             out[("per-rank base", lo, hi)] = D.stats(lo, hi, broadcast=False, backend=be, device=cpu)
+            out[("cost split", lo, hi)] = D.stats(lo, hi, broadcast=False, backend=be, device=cpu, split="cost")
         lo5, hi5 = inputs.config5_intervals(64)
         c, s = D.batch(lo5, hi5, batch_fn=lambda a, b: oracle.batch(a, b, 1), device=cpu)
         out["batch"] = (c.tolist(), s.tolist())
@@ -209,7 +210,7 @@ def test_two_rank_gloo_stats_batch_and_wrap():
             assert words == obm.tolist(), key                     # gathered bitmap == whole bitmap
             assert cs == D.bitmap_checksum(obm), key              # all-reduced decomposable checksum
             assert lst == oracle.primes(lo, hi).tolist(), key     # gathered list == whole list
-        elif isinstance(key, tuple) and key[0] in ("F4", "per-rank base"):
+        elif isinstance(key, tuple) and key[0] in ("F4", "per-rank base", "cost split"):
             assert val == oracle.stats(*key[1:]), key          # one reduction, whole range
         elif isinstance(key, tuple):
             assert val == oracle.stats(*key), key
@@ -221,11 +222,12 @@ def test_two_rank_gloo_stats_batch_and_wrap():
     assert r["wrap"] == 4
 
 
+@pytest.mark.parametrize("split", ["equal", "cost"])
 @pytest.mark.parametrize("G", [1, 2, 3, 4, 8, 13])
-def test_block_partition_tiles_range(G):
+def test_block_partition_tiles_range(G, split):
     for lo, hi in [(2, 10**10 + 1), (0, 1), (0, 0), (7, 7 + 64 * 5 + 3), (10**12, 10**12 + 10**10),
                    (123, 124), (1, 64 * 3)]:
-        blocks = [D.block_of(lo, hi, g, G) for g in range(G)]
+        blocks = [D.block_of(lo, hi, g, G, split) for g in range(G)]
         assert blocks[0][0] == lo and blocks[-1][1] == hi
         for (a0, b0), (a1, b1) in zip(blocks, blocks[1:]):
             assert b0 == a1 and a0 <= b0
@@ -241,11 +243,28 @@ def test_block_partition_matches_survey_g2():
     assert D.block_of(2, 10**10 + 1, 1, 2) == (5000000003, 10**10 + 1)
 
 
-def test_block_additivity_small():
-    lo, hi = 10**9, 10**9 + 4 * 10**6 + 7
+def test_cost_split_shape():
+    """split="cost": the low blocks of [2, 10^10] are longer than the high
+    ones (work per integer grows like ln ln x), monotonically; far from 0
+    (config 4) the blocks are equal to within 0.1 %; an unknown split raises."""
+    lo, hi = 2, 10**10 + 1
+    for G in (2, 4, 8):
+        w = [b - a for a, b in (D.block_of(lo, hi, g, G, "cost") for g in range(G))]
+        assert all(x > y for x, y in zip(w, w[1:])) and sum(w) == hi - lo
+        assert 1.0 < w[0] / w[-1] < 1.35
+    lo, hi = 10**12, 10**12 + 10**10
+    w = [b - a for a, b in (D.block_of(lo, hi, g, 8, "cost") for g in range(8))]
+    assert max(w) / min(w) < 1.001
+    with pytest.raises(ValueError):
+        D.block_of(2, 100, 0, 2, "lpt")
+
+
+@pytest.mark.parametrize("split", ["equal", "cost"])
+def test_block_additivity_small(split):
+    lo, hi = (10**9, 10**9 + 4 * 10**6 + 7) if split == "equal" else (2, 4 * 10**6 + 7)
     tot_c, tot_s = 0, 0
     for g in range(5):
-        a, b = D.block_of(lo, hi, g, 5)
+        a, b = D.block_of(lo, hi, g, 5, split)
         c, s = oracle.stats(a, b, 1)
         tot_c += c
         tot_s = (tot_s + s) & MASK64

@@ -275,6 +275,14 @@ def test_config3_count_sum_and_blocks():
             tot_c += c
             tot_s = (tot_s + s) & MASK64
         assert (tot_c, tot_s) == (int(PINS["config3.count"]), int(PINS["config3.sum"]))
+    # the cost-weighted split (dist.block_of split="cost") adds up as well
+    for G in (2, 8):
+        tot_c, tot_s = 0, 0
+        for g in range(G):
+            c, s = sv.stats(*block_of(lo, hi, g, G, "cost"))
+            tot_c += c
+            tot_s = (tot_s + s) & MASK64
+        assert (tot_c, tot_s) == (int(PINS["config3.count"]), int(PINS["config3.sum"]))
     # every block of G = 2, 4, 8 against tests/golden/config3_blocks.txt
     # (reproduced by the oracle in test_oracle_golden.py)
     for G, g, a, b, c, s in config3_blocks():

@@ -1,6 +1,7 @@
 """Per-rank sieve-kernel time and roofline fraction of config 3 split over G
 GPUs, measured one block at a time on one GPU (each rank's block is an
-independent range: the N>1 kernels do not interact until the all-reduce)."""
+independent range: the N>1 kernels do not interact until the all-reduce).
+Env: GS (default 1,2,4,8), SPLIT=equal|cost (dist.block_of), RANKS=ends|all."""
 import math, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -14,9 +15,10 @@ lo, hi = bench.CONFIG3
 r_atom, _ = sv.debug_k0()  # K0 on this GPU (lanes/clk/SM)
 peak = 148 * r_atom * 1965e6 / 1e9
 W = sv.get_options()["wheel"]
+SPLIT = os.environ.get("SPLIT", "equal")
 for G in [int(x) for x in os.environ.get("GS", "1,2,4,8").split(",")]:
-    for g in sorted({0, G - 1}):
-        a, b = D.block_of(lo, hi, g, G)
+    for g in (range(G) if os.environ.get("RANKS", "ends") == "all" else sorted({0, G - 1})):
+        a, b = D.block_of(lo, hi, g, G, SPLIT)
         r = math.isqrt(b - 1)
         base = D.alloc_base(sv.base_capacity(r), torch.device("cuda"))
         res = torch.zeros(2, dtype=torch.int64, device="cuda")
@@ -39,6 +41,6 @@ for G in [int(x) for x in os.environ.get("GS", "1,2,4,8").split(",")]:
                 fs.append(e[0].elapsed_time(e[1]))
         k = statistics.median(ks)
         m = bench.algorithmic_marks(a, b, W)
-        print(f"G={G} rank={g} [{a},{b}) K1={statistics.median(bs)*1e3:.1f}us sieve={k*1e3:.1f}us "
+        print(f"split={SPLIT} G={G} rank={g} [{a},{b}) K1={statistics.median(bs)*1e3:.1f}us sieve={k*1e3:.1f}us "
               f"frac={m / (k / 1e3) / 1e9 / peak:.3f} | K1+sieve={(statistics.median(bs) + k)*1e3:.1f}us "
               f"fused={statistics.median(fs)*1e3:.1f}us", flush=True)
