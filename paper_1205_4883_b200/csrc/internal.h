@@ -147,6 +147,9 @@ constexpr uint32_t kSmemAlign = 128;
 #ifndef SIEVE_WB_DIAG  // diagnostics builds only: 1 = no wait for the bulk copy's reads, 2 = no bulk copy, 3 = no transpose
 #define SIEVE_WB_DIAG 0
 #endif
+#ifndef SIEVE_LIST_STAGE  // A8 list emission staged in the consumed words of the segment: words per lane and pass (0 = direct)
+#define SIEVE_LIST_STAGE 4  // config 4 list, same box: 0 / 3 / 4 / 5 / 6 / 8 -> 2.834 / 2.542 / 2.512 / 2.525 / 2.528 / 2.614 ms
+#endif
 #ifndef SIEVE_LIST_WORDS  // A8 list emission: consecutive words per lane and warp pass (1 to 4)
 #define SIEVE_LIST_WORDS 1  // A/B on config 4 list: 1 / 2 / 3 / 4 -> 2.83 / 3.02 / 3.28 / 3.6 ms
 #endif

@@ -1442,7 +1442,7 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
   // 64-bit offsets per kLW words); their primes go out word by word
   constexpr uint32_t kLW = SIEVE_LIST_WORDS;
   static_assert(kLW >= 1 && kLW <= 4, "SIEVE_LIST_WORDS: 1 to 4");
-  for (uint32_t w0 = wb; w0 < we; w0 += 32u * kLW) {
+  auto emit_direct = [&](const uint32_t w0) {
     const uint32_t w = w0 + kLW * lane;
     uint32_t xs[kLW];
     uint32_t cx = 0;
@@ -1499,7 +1499,80 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
       }
     }
     base += __shfl_sync(0xffffffffu, incl, 31);
+  };
+#if SIEVE_LIST_STAGE
+  // Staged passes (internal.h SIEVE_LIST_STAGE): lane l takes kSW consecutive
+  // words of a pass of 32 kSW; one warp scan per pass; the lanes drop the
+  // 16-bit slot numbers of their primes (slot within the pass) in list order
+  // into the bytes of the warp's words already consumed -- up to a pass
+  // before this one and, once every lane holds its words in registers, this
+  // pass's own: 4 bytes per word, room for two primes per word -- and the warp
+  // then writes the pass's primes in order, two per lane and 16-byte store.
+  // The warp's first pass, a pass too dense for that room and a list that
+  // would overflow take the direct path.
+  static_assert(kLW == 1, "SIEVE_LIST_STAGE needs SIEVE_LIST_WORDS = 1");
+  constexpr uint32_t kSW = SIEVE_LIST_STAGE, kPW = 32u * kSW;
+  static_assert(kSW >= 2 && kSW <= 8, "SIEVE_LIST_STAGE: 2 to 8 words per lane");
+  uint32_t w0 = wb;
+  // direct until half a pass of the warp's words is consumed: with the
+  // pass's own words that is room for 3 primes per 2 words of the pass
+  for (; w0 < we && w0 < wb + kPW / 2u; w0 += 32u) emit_direct(w0);
+  for (; w0 < we; w0 += kPW) {
+    const uint32_t wl = w0 + kSW * lane;
+    uint32_t xs[kSW];
+    uint32_t cx = 0;
+#pragma unroll
+    for (uint32_t e = 0; e < kSW; ++e) {
+      xs[e] = wl + e < we ? ~seg[wl + e] : 0u;
+      cx += __popc(xs[e]);
+    }
+    uint32_t incl = cx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();  // every lane holds its words: the pass's bytes are free
+    const uint32_t st0 = w0 - wb >= kPW ? w0 - kPW : wb;       // first word of the staging area
+    const uint32_t room = 2u * (min(w0 + kPW, we) - st0);      // 16-bit entries
+    const uint32_t head = (uint32_t)(reinterpret_cast<uintptr_t>(P.list + base) >> 3) & 1u;
+    if (head + tot <= room && base + tot <= P.list_cap) {
+      // the staging area is shared memory reinterpreted as 16-bit entries
+      unsigned short *st = reinterpret_cast<unsigned short *>(const_cast<uint32_t *>(seg) + st0);
+      unsigned short *q = st + head + (incl - cx);
+#pragma unroll
+      for (uint32_t e = 0; e < kSW; ++e) {
+        uint32_t x = xs[e];
+        const uint32_t s16 = 32u * (kSW * lane + e);
+        while (x) {
+          *q++ = (unsigned short)(s16 + (uint32_t)(__ffs(x) - 1));
+          x &= x - 1;
+        }
+      }
+      __syncwarp();
+      const uint64_t v0 = a + 64ull * w0;  // slot 0 of the pass
+      uint64_t *dst = P.list + base;       // staged entry t goes to dst[t - head]
+      const uint32_t T = head + tot;
+      SV_CHECK(base + tot <= P.list_cap, kVioListStore);
+      for (uint32_t t = 2u * head + 2u * lane; t + 1u < T; t += 64u) {
+        const uint32_t pr = *reinterpret_cast<const uint32_t *>(st + t);
+        SV_CHECK((reinterpret_cast<uintptr_t>(dst + (t - head)) & 15u) == 0, kVioListStore);
+        *reinterpret_cast<ulonglong2 *>(dst + (t - head)) =
+            make_ulonglong2(v0 + 2ull * (pr & 0xFFFFu), v0 + 2ull * (pr >> 16));
+      }
+      if (lane == 0) {
+        if (head && tot) dst[0] = v0 + 2ull * st[1];
+        if (T > 2u * head && ((T - 2u * head) & 1u)) dst[T - 1u - head] = v0 + 2ull * st[T - 1u];
+      }
+      base += tot;
+    } else {
+      for (uint32_t u = w0; u < we && u < w0 + kPW; u += 32u) emit_direct(u);
+    }
   }
+#else
+  for (uint32_t w0 = wb; w0 < we; w0 += 32u * kLW) emit_direct(w0);
+#endif
   const uint64_t tot = s_wc[32];
   __syncthreads();  // s_wc is reused by the next segment
   return threadIdx.x == 0 ? tot : 0ull;  // counted once per CTA
