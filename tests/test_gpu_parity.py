@@ -177,6 +177,29 @@ def test_primes_list_truncation_and_device_out():
     assert cb == oc and np.array_equal(db.cpu().numpy().view(np.uint32), obm)
 
 
+@pytest.mark.parametrize("seg_kb,threads", [(8, 1024), (16, 1024), (16, 256), (32, 512), (208, 1024)])
+def test_list_staged_emission_edges(seg_kb, threads):
+    """A8 staged emission (kernels.cu list_emit, SIEVE_LIST_STAGE): warps whose
+    word range is shorter than half a pass (direct only), one partial staged
+    pass, many passes; ranges too dense for the staging room (direct
+    fallback pass by pass), ranges where dense and sparse passes mix, and
+    config 4's density; the list cut inside a staged pass, with guard
+    elements past the cap, at both 16-byte phases of the output."""
+    torch = pytest.importorskip("torch")
+    sv.set_options(segment_kb=seg_kb, threads=threads)
+    for lo, hi in [(2, 4 * 10**6 + 1), (3 * 10**3, 10**6), (10**7 + 1, 10**7 + 3 * 10**6),
+                   (10**12 + 11, 10**12 + 5 * 10**6)]:
+        full = oracle.primes(lo, hi)
+        for off in (0, 1):
+            for cap in (full.size, full.size - 37, full.size // 2 + 1):
+                d = torch.full((off + cap + 64,), -7, dtype=torch.int64, device="cuda")
+                _, c = sv.primes(lo, hi, cap=cap, out=d[off:off + cap])
+                h = d.cpu().numpy()
+                assert c == full.size
+                assert np.array_equal(h[off:off + cap].view(np.uint64), full[:cap]), (lo, hi, off, cap)
+                assert (h[:off] == -7).all() and (h[off + cap:] == -7).all(), (lo, hi, off, cap)
+
+
 @pytest.mark.parametrize("shift", [0, 1, 2, 3])
 def test_bitmap_bulk_copy_edges(shift):
     """A7 by TMA bulk copy (csrc/kernels.cu epilogue<kBitmap>): device outputs
