@@ -1543,12 +1543,25 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
       unsigned short *q = st + head + (incl - cx);
 #pragma unroll
       for (uint32_t e = 0; e < kSW; ++e) {
-        uint32_t x = xs[e];
         const uint32_t s16 = 32u * (kSW * lane + e);
+#if SIEVE_LIST_BFIND
+        // one BREV per word, then one FLO (bfind) per prime: the lowest set
+        // bit of x is the highest of y, at position 31 - b (BREV and FLO
+        // share the quarter-rate pipe, the loop's bound)
+        uint32_t y = __brev(xs[e]);
+        while (y) {
+          uint32_t f;
+          asm("bfind.u32 %0, %1;" : "=r"(f) : "r"(y));
+          *q++ = (unsigned short)(s16 + 31u - f);
+          y ^= 1u << f;
+        }
+#else
+        uint32_t x = xs[e];
         while (x) {
           *q++ = (unsigned short)(s16 + (uint32_t)(__ffs(x) - 1));
           x &= x - 1;
         }
+#endif
       }
       __syncwarp();
       const uint64_t v0 = a + 64ull * w0;  // slot 0 of the pass
