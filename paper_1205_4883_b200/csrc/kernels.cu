@@ -1500,7 +1500,10 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
     }
     base += __shfl_sync(0xffffffffu, incl, 31);
   };
-#if SIEVE_LIST_STAGE
+#if SIEVE_LIST_DIAG == 1
+  // diagnostics build: no pass 2 (wrong list) -- what the untranspose, the
+  // count pass and the look-back cost without the emission
+#elif SIEVE_LIST_STAGE
   // Staged passes (internal.h SIEVE_LIST_STAGE): lane l takes kSW consecutive
   // words of a pass of 32 kSW; one warp scan per pass; the lanes drop the
   // 16-bit slot numbers of their primes (slot within the pass) in list order
