@@ -150,6 +150,9 @@ constexpr uint32_t kSmemAlign = 128;
 #ifndef SIEVE_LIST_STAGE  // A8 list emission staged in the consumed words of the segment: words per lane and pass (0 = direct)
 #define SIEVE_LIST_STAGE 4  // config 4 list, same box: 0 / 3 / 4 / 5 / 6 / 8 -> 2.834 / 2.542 / 2.512 / 2.525 / 2.528 / 2.614 ms
 #endif
+#ifndef SIEVE_LIST_QUAD  // staged emission: four entries per lane and step of the ordered write (else two)
+#define SIEVE_LIST_QUAD 0
+#endif
 #ifndef SIEVE_LIST_DIAG  // 1: list mode without pass 2 (diagnostics build, wrong list)
 #define SIEVE_LIST_DIAG 0
 #endif

@@ -1537,13 +1537,24 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
     }
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
     __syncwarp();  // every lane holds its words: the pass's bytes are free
-    const uint32_t st0 = w0 - wb >= kPW ? w0 - kPW : wb;       // first word of the staging area
+    uint32_t st0 = w0 - wb >= kPW ? w0 - kPW : wb;             // first word of the staging area
+#if SIEVE_LIST_QUAD
+    st0 += st0 & 1u;  // 8-byte aligned (the segment is 128-byte aligned)
+#endif
     const uint32_t room = 2u * (min(w0 + kPW, we) - st0);      // 16-bit entries
     const uint32_t head = (uint32_t)(reinterpret_cast<uintptr_t>(P.list + base) >> 3) & 1u;
-    if (head + tot <= room && base + tot <= P.list_cap) {
+#if SIEVE_LIST_QUAD
+    // four entries per lane and step of the ordered write (one 8-byte load,
+    // two 16-byte stores): the odd first prime sits at entry 3, so that the
+    // aligned part starts at entry 4 (8-byte aligned in the staging area)
+    const uint32_t off = 3u * head;
+#else
+    const uint32_t off = head;
+#endif
+    if (off + tot <= room && base + tot <= P.list_cap) {
       // the staging area is shared memory reinterpreted as 16-bit entries
       unsigned short *st = reinterpret_cast<unsigned short *>(const_cast<uint32_t *>(seg) + st0);
-      unsigned short *q = st + head + (incl - cx);
+      unsigned short *q = st + off + (incl - cx);
 #pragma unroll
       for (uint32_t e = 0; e < kSW; ++e) {
         const uint32_t s16 = 32u * (kSW * lane + e);
@@ -1568,18 +1579,32 @@ __device__ __forceinline__ uint64_t list_emit(const uint32_t *seg, uint64_t s, u
       }
       __syncwarp();
       const uint64_t v0 = a + 64ull * w0;  // slot 0 of the pass
-      uint64_t *dst = P.list + base;       // staged entry t goes to dst[t - head]
-      const uint32_t T = head + tot;
+      uint64_t *dst = P.list + base;       // staged entry t goes to dst[t - off]
+      const uint32_t T = off + tot, t0 = off + head;  // the aligned part: entries [t0, T)
       SV_CHECK(base + tot <= P.list_cap, kVioListStore);
-      for (uint32_t t = 2u * head + 2u * lane; t + 1u < T; t += 64u) {
+#if SIEVE_LIST_QUAD
+      constexpr uint32_t kQ = 4;
+      for (uint32_t t = t0 + kQ * lane; t + (kQ - 1u) < T; t += 32u * kQ) {
+        const uint2 pr = *reinterpret_cast<const uint2 *>(st + t);
+        SV_CHECK((reinterpret_cast<uintptr_t>(dst + (t - off)) & 15u) == 0, kVioListStore);
+        ulonglong2 *d2 = reinterpret_cast<ulonglong2 *>(dst + (t - off));
+        d2[0] = make_ulonglong2(v0 + 2ull * (pr.x & 0xFFFFu), v0 + 2ull * (pr.x >> 16));
+        d2[1] = make_ulonglong2(v0 + 2ull * (pr.y & 0xFFFFu), v0 + 2ull * (pr.y >> 16));
+      }
+#else
+      constexpr uint32_t kQ = 2;
+      for (uint32_t t = t0 + kQ * lane; t + (kQ - 1u) < T; t += 32u * kQ) {
         const uint32_t pr = *reinterpret_cast<const uint32_t *>(st + t);
-        SV_CHECK((reinterpret_cast<uintptr_t>(dst + (t - head)) & 15u) == 0, kVioListStore);
-        *reinterpret_cast<ulonglong2 *>(dst + (t - head)) =
+        SV_CHECK((reinterpret_cast<uintptr_t>(dst + (t - off)) & 15u) == 0, kVioListStore);
+        *reinterpret_cast<ulonglong2 *>(dst + (t - off)) =
             make_ulonglong2(v0 + 2ull * (pr & 0xFFFFu), v0 + 2ull * (pr >> 16));
       }
-      if (lane == 0) {
-        if (head && tot) dst[0] = v0 + 2ull * st[1];
-        if (T > 2u * head && ((T - 2u * head) & 1u)) dst[T - 1u - head] = v0 + 2ull * st[T - 1u];
+#endif
+      // the odd first prime and the last (T - t0) mod kQ, one lane each
+      if (lane == 31u && head && tot) dst[0] = v0 + 2ull * st[off];
+      if (T > t0) {
+        const uint32_t rem = (T - t0) % kQ, tt = T - rem;
+        if (lane < rem) dst[tt + lane - off] = v0 + 2ull * st[tt + lane];
       }
       base += tot;
     } else {
